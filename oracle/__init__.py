@@ -69,6 +69,14 @@ def _load():
         lib.oracle_colorize.restype = i32
         lib.oracle_cardioid_point.argtypes = [f64, f64, ctypes.POINTER(f64), ctypes.POINTER(f64)]
         lib.oracle_cardioid_point.restype = None
+        lib.oracle_distance_estimate.argtypes = [i32, f64, f64, f64, f64, ctypes.c_long]
+        lib.oracle_distance_estimate.restype = f64
+        lib.oracle_distance_pixels.argtypes = [i32, f64, f64, f64, f64, f64, f64, i64, i64, vp, vp,
+                                               i64, ctypes.c_long, vp]
+        lib.oracle_distance_pixels.restype = i32
+        lib.oracle_pixels_nudged.argtypes = [i32, f64, f64, f64, f64, f64, f64, i64, i64, i32, i32,
+                                             vp, vp, i64, i32, vp]
+        lib.oracle_pixels_nudged.restype = i32
         _lib = lib
         return lib
 
@@ -179,4 +187,43 @@ def colorize(counts: np.ndarray, max_iter: int, palette: np.ndarray, interior) -
                                  _ptr(inter), _ptr(out))
     if rc != 0:
         raise ValueError("oracle_colorize: invalid arguments")
+    return out
+
+
+# --------------------------------------------------------------------------- fast-mode tools
+def distance_estimate(kind: str, z0: complex, c: complex, max_iter: int = 1_000_000) -> float:
+    """Exterior distance estimate |Z| ln|Z| / |Z'| (binary64, bailout 1e10); 0 if the
+    orbit does not escape (reading c-10).  kind 'julia' (derivative in Z_0)
+    or 'mandelbrot' (derivative in c, Z_0 = 0)."""
+    m = {"julia": 0, "mandelbrot": 1}[kind]
+    return float(_load().oracle_distance_estimate(m, z0.real, z0.imag, c.real, c.imag, max_iter))
+
+
+def distance_pixels(kind: str, c: complex, center: complex, half_w: float, half_h: float,
+                    width: int, height: int, px, py, max_iter: int = 1_000_000) -> np.ndarray:
+    px = np.ascontiguousarray(px, dtype=np.int64)
+    py = np.ascontiguousarray(py, dtype=np.int64)
+    out = np.empty(px.shape, dtype=np.float64)
+    m = {"julia": 0, "mandelbrot": 1}[kind]
+    rc = _load().oracle_distance_pixels(m, c.real, c.imag, center.real, center.imag, half_w,
+                                        half_h, width, height, _ptr(px), _ptr(py), px.size,
+                                        max_iter, _ptr(out))
+    if rc != 0:
+        raise ValueError("oracle_distance_pixels: invalid arguments")
+    return out
+
+
+def pixels_nudged(kind: str, c: complex, center: complex, half_w: float, half_h: float,
+                  width: int, height: int, max_iter: int, precision, px, py,
+                  nudge: int = 1) -> np.ndarray:
+    """Strict counts with the start value's real part moved by `nudge` ulps."""
+    px = np.ascontiguousarray(px, dtype=np.int64)
+    py = np.ascontiguousarray(py, dtype=np.int64)
+    out = np.empty(px.shape, dtype=np.uint16)
+    m = {"julia": 0, "mandelbrot": 1}[kind]
+    rc = _load().oracle_pixels_nudged(m, c.real, c.imag, center.real, center.imag, half_w, half_h,
+                                      width, height, max_iter, _prec(precision), _ptr(px),
+                                      _ptr(py), px.size, nudge, _ptr(out))
+    if rc != 0:
+        raise ValueError("oracle_pixels_nudged: invalid arguments")
     return out

@@ -267,3 +267,80 @@ void oracle_cardioid_point(double t, double a, double* re, double* im) {
     *re = (2.0 * cos(t) - cos(2.0 * t)) / a;
     *im = (2.0 * sin(t) - sin(2.0 * t)) / a;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Fast-mode tolerance tools (reading c-10).                        */
+/* ------------------------------------------------------------------------- */
+
+/* Distance estimate DE = |Z_n| ln|Z_n| / |Z'_n| in binary64 (standard exterior
+ * distance estimator; Koebe-type bound: distance to the set boundary >= DE/2).
+ * Julia: Z_0 = z0, Z'_0 = 1, Z'_{k+1} = 2 Z_k Z'_k.  Mandelbrot: Z_0 = 0, Z'_0 = 0,
+ * Z'_{k+1} = 2 Z_k Z'_k + 1 (derivative in c).  Bailout |Z|^2 > 1e20; returns 0 if
+ * the orbit has not escaped after max_iter iterations (treated as "in the set"). */
+double oracle_distance_estimate(int mandel, double zre, double zim, double cre, double cim,
+                                long max_iter) {
+    double x = mandel ? 0.0 : zre, y = mandel ? 0.0 : zim;
+    double dx = mandel ? 0.0 : 1.0, dy = 0.0;
+    for (long n = 0; n < max_iter; ++n) {
+        double m = x * x + y * y;
+        if (m > 1e20) {
+            double r = sqrt(m);
+            double dr = sqrt(dx * dx + dy * dy);
+            return r * log(r) / dr;
+        }
+        /* Z' <- 2 Z Z' (+1 for Mandelbrot), using the old Z */
+        double ndx = 2.0 * (x * dx - y * dy) + (mandel ? 1.0 : 0.0);
+        double ndy = 2.0 * (x * dy + y * dx);
+        dx = ndx;
+        dy = ndy;
+        double nx = x * x - y * y + cre;
+        double ny = 2.0 * x * y + cim;
+        x = nx;
+        y = ny;
+    }
+    return 0.0;
+}
+
+/* DE at selected pixel centres (exact binary64 pixel centres, reading c-3). */
+int oracle_distance_pixels(int mandel, double c_re, double c_im, double center_re,
+                           double center_im, double half_w, double half_h, int64_t width,
+                           int64_t height, const int64_t* px, const int64_t* py, int64_t n_pix,
+                           long max_iter, double* out) {
+    if (width < 1 || height < 1 || n_pix < 0) return -1;
+    for (int64_t i = 0; i < n_pix; ++i) {
+        if (px[i] < 0 || px[i] >= width || py[i] < 0 || py[i] >= height) return -1;
+        double re = oracle_pixel_re(center_re, half_w, width, px[i]);
+        double im = oracle_pixel_im(center_im, half_h, height, py[i]);
+        out[i] = mandel ? oracle_distance_estimate(1, 0.0, 0.0, re, im, max_iter)
+                        : oracle_distance_estimate(0, re, im, c_re, c_im, max_iter);
+    }
+    return 0;
+}
+
+/* Strict counts at selected pixels with the pixel's start value (Julia Z_0, or the
+ * Mandelbrot C) real part moved by `nudge` ulps of the working precision: the
+ * problem's own 1-ulp sensitivity, against which fast-mode differences are judged. */
+int oracle_pixels_nudged(int mandel, double c_re, double c_im, double center_re,
+                         double center_im, double half_w, double half_h, int64_t width,
+                         int64_t height, int max_iter, int precision, const int64_t* px,
+                         const int64_t* py, int64_t n_pix, int nudge, uint16_t* out) {
+    if (!args_ok(precision, width, height, max_iter) || n_pix < 0) return -1;
+    for (int64_t i = 0; i < n_pix; ++i) {
+        if (px[i] < 0 || px[i] >= width || py[i] < 0 || py[i] >= height) return -1;
+        double re = oracle_pixel_re(center_re, half_w, width, px[i]);
+        double im = oracle_pixel_im(center_im, half_h, height, py[i]);
+        if (precision == 32) {
+            float r = (float)re;
+            for (int k = 0; k < nudge; ++k) r = nextafterf(r, INFINITY);
+            out[i] = (uint16_t)(mandel ? oracle_escape_f32(0.0f, 0.0f, r, (float)im, max_iter)
+                                       : oracle_escape_f32(r, (float)im, (float)c_re,
+                                                           (float)c_im, max_iter));
+        } else {
+            double r = re;
+            for (int k = 0; k < nudge; ++k) r = nextafter(r, INFINITY);
+            out[i] = (uint16_t)(mandel ? oracle_escape_f64(0.0, 0.0, r, im, max_iter)
+                                       : oracle_escape_f64(r, im, c_re, c_im, max_iter));
+        }
+    }
+    return 0;
+}

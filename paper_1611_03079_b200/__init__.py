@@ -9,7 +9,8 @@ library is missing (there is no CPU fallback).
 from importlib import import_module as _imp
 
 __all__ = ["julia_render", "julia_render_ex", "julia_render_path", "mandelbrot_param_map",
-           "colorize", "FractalError", "Mode", "Bands", "band_local_rows", "workloads"]
+           "colorize", "FractalError", "Mode", "Bands", "FULL_FRAME", "band_local_rows",
+           "band_global_row", "launch_count", "version", "workloads"]
 
 
 def __getattr__(name):

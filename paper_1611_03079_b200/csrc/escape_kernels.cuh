@@ -1,0 +1,307 @@
+// escape_kernels.cuh -- sm_100a device code for the escape-time hot path.
+//
+// Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, "reading c-k" = DESIGN.md
+// §Readings.  Nothing here is shared with oracle/ (which is plain C, test-only).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fr {
+
+constexpr int kThreads = 256;      // 8 warps per CTA
+constexpr int kTileW = 32;         // CTA tile: 32 x 8 pixels, one pixel per thread
+constexpr int kTileH = 8;
+constexpr int kWarpW = 8;          // warp tile: 8 x 4 pixels (2-D for orbit coherence)
+constexpr int kWarpH = 4;
+constexpr int kMaxPathChunk = 1024;  // C values per launch, carried in kernel params
+constexpr unsigned kFull = 0xffffffffu;
+
+// ----------------------------------------------------------------------------------
+// Parameters (passed by value; the path chunk's C values ride in param space).
+// ----------------------------------------------------------------------------------
+struct Palette {
+  uchar4 e[256];
+  uchar4 interior;
+  uint32_t n;      // entries, 2..256
+  uint32_t magic;  // ceil(2^32 / n): count mod n = c - n * umulhi(c, magic) for c < 2^16
+};
+
+struct Geom {
+  double cx, cy;  // window centre
+  double hx, hy;  // half_w / W, half_h / H (rounded once on the host, reading c-3)
+  int W, H;       // full-frame size
+  int rows;       // rows held by this call (bands) -- output has rows x W per frame
+  int band_rows, n_ranks, rank;  // cyclic bands (band_rows == 0: rows == H, identity)
+  int max_iter;
+  int tiles_x;    // ceil(W / kTileW)
+  int64_t frame_stride;  // rows * W
+  uint16_t* counts;
+  uchar4* rgba;   // nullptr unless colour levels are fused
+};
+
+template <int NC>
+struct CList {
+  double2 c[NC];
+};
+
+// ----------------------------------------------------------------------------------
+// Region-covering map, reading c-3: pixel centres, row 0 at the top, binary64
+// with each operation separately rounded (explicit _rn intrinsics: no contraction).
+// ----------------------------------------------------------------------------------
+__device__ __forceinline__ double pixel_re(const Geom& g, int px) {
+  const double k = (double)(2 * (long long)px + 1 - g.W);
+  return __dadd_rn(g.cx, __dmul_rn(k, g.hx));
+}
+__device__ __forceinline__ double pixel_im(const Geom& g, int gy) {
+  const double k = (double)((long long)g.H - 1 - 2 * (long long)gy);
+  return __dadd_rn(g.cy, __dmul_rn(k, g.hy));
+}
+
+// Local output row -> global frame row under cyclic bands.
+__device__ __forceinline__ int global_row(const Geom& g, int ly) {
+  if (g.band_rows == 0) return ly;
+  const int b = ly / g.band_rows;
+  const int w = ly - b * g.band_rows;
+  return (b * g.n_ranks + g.rank) * g.band_rows + w;
+}
+
+// ----------------------------------------------------------------------------------
+// Sticky "alive" predicate + predicated count increment, one FSETP/DSETP and one
+// predicated IADD per iteration (the SASS is FSETP.LE.AND P, PT, m, lim, P and
+// @P IADD3).  cnt ends as the number of leading iterations n with |Z_n|^2 <= 4,
+// which is the escape count when the loop ran >= max_iter iterations (clamped).
+// ----------------------------------------------------------------------------------
+__device__ __forceinline__ void alive_step_f32(unsigned& alive, int& cnt, float m, float lim) {
+  asm("{\n\t.reg .pred pa, pb;\n\t"
+      "setp.ne.u32 pa, %1, 0;\n\t"
+      "setp.le.and.f32 pb, %2, %3, pa;\n\t"
+      "selp.u32 %1, 1, 0, pb;\n\t"
+      "@pb add.s32 %0, %0, 1;\n\t}"
+      : "+r"(cnt), "+r"(alive)
+      : "f"(m), "f"(lim));
+}
+__device__ __forceinline__ void alive_step_f64(unsigned& alive, int& cnt, double m, double lim) {
+  asm("{\n\t.reg .pred pa, pb;\n\t"
+      "setp.ne.u32 pa, %1, 0;\n\t"
+      "setp.le.and.f64 pb, %2, %3, pa;\n\t"
+      "selp.u32 %1, 1, 0, pb;\n\t"
+      "@pb add.s32 %0, %0, 1;\n\t}"
+      : "+r"(cnt), "+r"(alive)
+      : "d"(m), "d"(lim));
+}
+
+// ----------------------------------------------------------------------------------
+// One iteration Z <- Z^2 + C with the escape test on Z (before the update).
+//
+// STRICT (reading c-9): exactly the oracle's sequence
+//   xx = x*x; yy = y*y; m = xx + yy; [m > 4 ?]; xy = x*y; x = (xx - yy) + cr;
+//   y = (xy + xy) + ci
+// with every op separately rounded (_rn intrinsics forbid contraction).
+//
+// FAST: state rescaled by 2, X = 2x, Y = 2y, with
+// CR2 = 2cr, CI2 = 2ci, so that
+//   Y' = 2(2xy + ci) = X*Y + CI2                 (one FFMA)
+//   X' = 2(x^2 - y^2 + cr) = (X^2 - Y^2)/2 + CR2 (FMUL, FFMA, FFMA-by-0.5)
+//   |Z|^2 > 4  <=>  X^2 + Y^2 > 16               (one FFMA)
+// i.e. 5 FP-pipe instructions per iteration instead of 6 unscaled.
+// ----------------------------------------------------------------------------------
+template <class T, bool STRICT>
+struct Iter;
+
+template <>
+struct Iter<float, true> {
+  static constexpr float kLim = 4.0f;
+  __device__ __forceinline__ static void step(float& x, float& y, float cr, float ci,
+                                              unsigned& alive, int& cnt) {
+    const float xx = __fmul_rn(x, x);
+    const float yy = __fmul_rn(y, y);
+    const float m = __fadd_rn(xx, yy);
+    alive_step_f32(alive, cnt, m, kLim);
+    const float xy = __fmul_rn(x, y);
+    const float t = __fsub_rn(xx, yy);
+    const float s = __fadd_rn(xy, xy);
+    x = __fadd_rn(t, cr);
+    y = __fadd_rn(s, ci);
+  }
+};
+
+template <>
+struct Iter<float, false> {
+  static constexpr float kLim = 16.0f;
+  __device__ __forceinline__ static void step(float& X, float& Y, float CR2, float CI2,
+                                              unsigned& alive, int& cnt) {
+    const float YY = __fmul_rn(Y, Y);
+    const float M = __fmaf_rn(X, X, YY);
+    alive_step_f32(alive, cnt, M, kLim);
+    const float Tm = __fmaf_rn(X, X, -YY);
+    const float Yn = __fmaf_rn(X, Y, CI2);
+    X = __fmaf_rn(Tm, 0.5f, CR2);
+    Y = Yn;
+  }
+};
+
+template <>
+struct Iter<double, true> {
+  static constexpr double kLim = 4.0;
+  __device__ __forceinline__ static void step(double& x, double& y, double cr, double ci,
+                                              unsigned& alive, int& cnt) {
+    const double xx = __dmul_rn(x, x);
+    const double yy = __dmul_rn(y, y);
+    const double m = __dadd_rn(xx, yy);
+    alive_step_f64(alive, cnt, m, kLim);
+    const double xy = __dmul_rn(x, y);
+    const double t = __dsub_rn(xx, yy);
+    const double s = __dadd_rn(xy, xy);
+    x = __dadd_rn(t, cr);
+    y = __dadd_rn(s, ci);
+  }
+};
+
+template <>
+struct Iter<double, false> {
+  static constexpr double kLim = 16.0;
+  __device__ __forceinline__ static void step(double& X, double& Y, double CR2, double CI2,
+                                              unsigned& alive, int& cnt) {
+    const double YY = __dmul_rn(Y, Y);
+    const double M = __fma_rn(X, X, YY);
+    alive_step_f64(alive, cnt, M, kLim);
+    const double Tm = __fma_rn(X, X, -YY);
+    const double Yn = __fma_rn(X, Y, CI2);
+    X = __fma_rn(Tm, 0.5, CR2);
+    Y = Yn;
+  }
+};
+
+// Initial state for a pixel: STRICT keeps (x, y, cr, ci); FAST keeps the doubled
+// values (exact scaling by 2).  For binary32 the binary64 map value and C are rounded
+// once to nearest (reading c-8).
+template <class T, bool STRICT>
+__device__ __forceinline__ T to_state(double v) {
+  const T t = (T)v;  // cvt.rn
+  return STRICT ? t : t + t;
+}
+
+// Count -> colour level: interior if count == max_iter, else
+// palette[count mod n].
+__device__ __forceinline__ uchar4 colour_of(const uchar4* spal, const Palette& p, int cnt,
+                                            int max_iter) {
+  if (cnt == max_iter) return p.interior;
+  const unsigned c = (unsigned)cnt;
+  const unsigned q = __umulhi(c, p.magic);
+  return spal[c - q * p.n];
+}
+
+// ----------------------------------------------------------------------------------
+// Static-tile kernel: one pixel per thread, 8x4 warp tiles, iteration in unrolled
+// blocks of K with a warp-vote (__any_sync) exit.  blockIdx.x = tile, blockIdx.y =
+// frame of the path chunk (C = cs.c[blockIdx.y]); MANDEL takes C from the pixel and
+// Z_0 = 0.
+// ----------------------------------------------------------------------------------
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int NC>
+__global__ void __launch_bounds__(kThreads)
+escape_tile_kernel(const Geom g, const Palette pal, const CList<NC> cs, int frame0) {
+  __shared__ uchar4 spal[COLOR ? 256 : 1];
+  if (COLOR) {
+    spal[threadIdx.x] = pal.e[threadIdx.x];
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int tile = blockIdx.x;
+  const int ty = tile / g.tiles_x;
+  const int tx = tile - ty * g.tiles_x;
+  const int px = tx * kTileW + (warp & 3) * kWarpW + (lane & 7);
+  const int ly = ty * kTileH + (warp >> 2) * kWarpH + (lane >> 3);
+  const bool inside = (px < g.W) && (ly < g.rows);
+  const int f = blockIdx.y;
+
+  T x, y, cr, ci;
+  {
+    const int gy = global_row(g, inside ? ly : 0);
+    const double re = pixel_re(g, inside ? px : 0);
+    const double im = pixel_im(g, gy);
+    if (MANDEL) {
+      x = T(0);
+      y = T(0);
+      cr = to_state<T, STRICT>(re);
+      ci = to_state<T, STRICT>(im);
+    } else {
+      x = to_state<T, STRICT>(re);
+      y = to_state<T, STRICT>(im);
+      const double2 c = cs.c[NC == 1 ? 0 : f];
+      cr = to_state<T, STRICT>(c.x);
+      ci = to_state<T, STRICT>(c.y);
+    }
+  }
+
+  unsigned alive = inside ? 1u : 0u;
+  int cnt = 0;
+  const int max_iter = g.max_iter;
+  int n = 0;
+  bool more = true;
+  while (n + K <= max_iter) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
+    n += K;
+    if (!__any_sync(kFull, alive)) {
+      more = false;
+      break;
+    }
+  }
+  if (more) {
+    for (; n < max_iter; ++n) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
+  }
+  if (!inside) return;
+  const int count = cnt < max_iter ? cnt : max_iter;
+  const int64_t off = (int64_t)(frame0 + f) * g.frame_stride + (int64_t)ly * g.W + px;
+  g.counts[off] = (uint16_t)count;
+  if (COLOR) g.rgba[off] = colour_of(spal, pal, count, max_iter);
+}
+
+// ----------------------------------------------------------------------------------
+// Standalone colour levels (N6): HBM-bound, 8 pixels per thread per step: one 16-byte
+// load of counts, two 16-byte stores of RGBA; grid-stride over 8-pixel groups.
+// ----------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+colorize_kernel(const uint16_t* __restrict__ counts, int64_t n_pixels, int max_iter,
+                const Palette pal, uchar4* __restrict__ rgba) {
+  __shared__ uchar4 spal[256];
+  spal[threadIdx.x] = pal.e[threadIdx.x];
+  __syncthreads();
+  const int64_t groups = n_pixels >> 3;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint4* __restrict__ c8 = reinterpret_cast<const uint4*>(counts);
+  uint4* __restrict__ o8 = reinterpret_cast<uint4*>(rgba);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < groups; i += stride) {
+    const uint4 v = __ldcs(c8 + i);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uchar4 a = colour_of(spal, pal, (int)(w[k] & 0xffffu), max_iter);
+      const uchar4 b = colour_of(spal, pal, (int)(w[k] >> 16), max_iter);
+      o[2 * k] = (uint32_t)a.x | ((uint32_t)a.y << 8) | ((uint32_t)a.z << 16) | ((uint32_t)a.w << 24);
+      o[2 * k + 1] = (uint32_t)b.x | ((uint32_t)b.y << 8) | ((uint32_t)b.z << 16) | ((uint32_t)b.w << 24);
+    }
+    __stcs(o8 + 2 * i, make_uint4(o[0], o[1], o[2], o[3]));
+    __stcs(o8 + 2 * i + 1, make_uint4(o[4], o[5], o[6], o[7]));
+  }
+  // ragged tail (< 8 pixels)
+  const int64_t t0 = groups << 3;
+  const int64_t t = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.x == 0 && t < n_pixels) rgba[t] = colour_of(spal, pal, counts[t], max_iter);
+}
+
+// Unaligned fallback (pointers not 16-byte aligned): one pixel per thread-step.
+__global__ void __launch_bounds__(kThreads)
+colorize_scalar_kernel(const uint16_t* __restrict__ counts, int64_t n_pixels, int max_iter,
+                       const Palette pal, uchar4* __restrict__ rgba) {
+  __shared__ uchar4 spal[256];
+  spal[threadIdx.x] = pal.e[threadIdx.x];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pixels; i += stride)
+    rgba[i] = colour_of(spal, pal, counts[i], max_iter);
+}
+
+}  // namespace fr

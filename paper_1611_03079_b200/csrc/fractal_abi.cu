@@ -1,0 +1,273 @@
+// fractal_abi.cu -- libfractal: the C ABI of include/fractal.h on top of the sm_100a
+// kernels in escape_kernels.cuh.  Host side: validation, binary64 parameter
+// derivation, chunking of C-paths into kernel parameters, dispatch.
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+
+#include "../../include/fractal.h"
+#include "escape_kernels.cuh"
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+thread_local int32_t g_last_cuda_error = 0;
+
+constexpr int64_t kMaxFramePixels = int64_t(1) << 31;  // S:182 resource limit
+
+inline bool is_fin(double v) { return std::isfinite(v); }
+
+fr_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return FR_OK;
+  g_last_cuda_error = (int32_t)e;
+  return FR_ERR_CUDA;
+}
+
+fr_status check_frame(fr_window win, int32_t width, int32_t height, int32_t max_iter) {
+  if (width < 1 || height < 1) return FR_ERR_INVALID_ARG;
+  if (!(is_fin(win.center_re) && is_fin(win.center_im) && is_fin(win.half_w) &&
+        is_fin(win.half_h)))
+    return FR_ERR_INVALID_ARG;
+  if (!(win.half_w > 0.0) || !(win.half_h > 0.0)) return FR_ERR_INVALID_ARG;
+  if (max_iter < 1) return FR_ERR_INVALID_ARG;
+  if (max_iter > 65535) return FR_ERR_UNSUPPORTED;
+  if ((int64_t)width * (int64_t)height > kMaxFramePixels) return FR_ERR_TOO_LARGE;
+  return FR_OK;
+}
+
+bool bands_valid(int32_t height, fr_bands b) {
+  (void)height;
+  return b.band_rows >= 0 && b.n_ranks >= 1 && b.rank >= 0 && b.rank < b.n_ranks &&
+         (b.band_rows > 0 || (b.n_ranks == 1 && b.rank == 0));
+}
+
+int64_t local_rows(int32_t height, fr_bands b) {
+  if (!bands_valid(height, b)) return -1;
+  if (b.band_rows == 0) return height;
+  const int64_t nb = ((int64_t)height + b.band_rows - 1) / b.band_rows;
+  int64_t rows = 0;
+  for (int64_t band = b.rank; band < nb; band += b.n_ranks) {
+    const int64_t r0 = band * b.band_rows;
+    const int64_t r1 = r0 + b.band_rows < height ? r0 + b.band_rows : height;
+    rows += r1 - r0;
+  }
+  return rows;
+}
+
+fr_status make_palette(const fr_palette* pal, fr::Palette* out) {
+  std::memset(out, 0, sizeof(*out));
+  if (!pal) return FR_OK;
+  if (!pal->rgba || pal->n < 2 || pal->n > 256) return FR_ERR_INVALID_ARG;
+  for (int i = 0; i < pal->n; ++i)
+    out->e[i] = make_uchar4(pal->rgba[4 * i], pal->rgba[4 * i + 1], pal->rgba[4 * i + 2],
+                            pal->rgba[4 * i + 3]);
+  out->interior = make_uchar4(pal->interior[0], pal->interior[1], pal->interior[2],
+                              pal->interior[3]);
+  out->n = (uint32_t)pal->n;
+  out->magic = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)pal->n - 1) / (uint64_t)pal->n);
+  return FR_OK;
+}
+
+// Parameter derivation in binary64: hx = half_w / W, hy = half_h / H.
+fr::Geom make_geom(fr_window win, int32_t width, int32_t height, int32_t max_iter,
+                   fr_bands b, int64_t rows, uint16_t* counts, uint8_t* rgba) {
+  fr::Geom g;
+  g.cx = win.center_re;
+  g.cy = win.center_im;
+  g.hx = win.half_w / (double)width;
+  g.hy = win.half_h / (double)height;
+  g.W = width;
+  g.H = height;
+  g.rows = (int)rows;
+  g.band_rows = b.band_rows;
+  g.n_ranks = b.n_ranks;
+  g.rank = b.rank;
+  g.max_iter = max_iter;
+  g.tiles_x = (width + fr::kTileW - 1) / fr::kTileW;
+  g.frame_stride = rows * (int64_t)width;
+  g.counts = counts;
+  g.rgba = reinterpret_cast<uchar4*>(rgba);
+  return g;
+}
+
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int NC>
+cudaError_t launch_tiles_t(const fr::Geom& g, const fr::Palette& pal, const fr::CList<NC>& cs,
+                           int n_frames, int frame0, cudaStream_t s) {
+  constexpr int K = 8;
+  const int64_t tiles = (int64_t)g.tiles_x * ((g.rows + fr::kTileH - 1) / fr::kTileH);
+  dim3 grid((unsigned)tiles, (unsigned)n_frames, 1);
+  fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, K, NC>
+      <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+template <bool MANDEL, bool COLOR, int NC>
+cudaError_t launch_tiles_mode(fr_mode mode, const fr::Geom& g, const fr::Palette& pal,
+                              const fr::CList<NC>& cs, int n_frames, int frame0,
+                              cudaStream_t s) {
+  switch (mode) {
+    case FR_FP32_FAST:
+      return launch_tiles_t<float, false, MANDEL, COLOR, NC>(g, pal, cs, n_frames, frame0, s);
+    case FR_FP32_STRICT:
+      return launch_tiles_t<float, true, MANDEL, COLOR, NC>(g, pal, cs, n_frames, frame0, s);
+    case FR_FP64_FAST:
+      return launch_tiles_t<double, false, MANDEL, COLOR, NC>(g, pal, cs, n_frames, frame0, s);
+    case FR_FP64_STRICT:
+      return launch_tiles_t<double, true, MANDEL, COLOR, NC>(g, pal, cs, n_frames, frame0, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <bool MANDEL, int NC>
+cudaError_t launch_tiles(fr_mode mode, bool color, const fr::Geom& g, const fr::Palette& pal,
+                         const fr::CList<NC>& cs, int n_frames, int frame0, cudaStream_t s) {
+  if (color) return launch_tiles_mode<MANDEL, true, NC>(mode, g, pal, cs, n_frames, frame0, s);
+  return launch_tiles_mode<MANDEL, false, NC>(mode, g, pal, cs, n_frames, frame0, s);
+}
+
+bool mode_valid(fr_mode m) {
+  return m == FR_FP32_FAST || m == FR_FP32_STRICT || m == FR_FP64_FAST || m == FR_FP64_STRICT;
+}
+
+fr_status render_frame(bool mandel, fr_complex c, fr_window win, int32_t width, int32_t height,
+                       int32_t max_iter, fr_mode mode, fr_bands bands, uint16_t* out_counts,
+                       const fr_palette* pal, uint8_t* out_rgba, fr_stream stream) {
+  fr_status st = check_frame(win, width, height, max_iter);
+  if (st != FR_OK) return st;
+  if (!mode_valid(mode)) return FR_ERR_UNSUPPORTED;
+  if (!mandel && !(is_fin(c.re) && is_fin(c.im))) return FR_ERR_INVALID_ARG;
+  if (!out_counts) return FR_ERR_INVALID_ARG;
+  if ((pal != nullptr) != (out_rgba != nullptr)) return FR_ERR_INVALID_ARG;
+  const int64_t rows = local_rows(height, bands);
+  if (rows < 0) return FR_ERR_INVALID_ARG;
+  fr::Palette p;
+  st = make_palette(pal, &p);
+  if (st != FR_OK) return st;
+  if (rows == 0) return FR_OK;  // this rank holds no band
+  const fr::Geom g = make_geom(win, width, height, max_iter, bands, rows, out_counts, out_rgba);
+  fr::CList<1> cs;
+  cs.c[0] = make_double2(c.re, c.im);
+  cudaError_t e = mandel ? launch_tiles<true, 1>(mode, pal != nullptr, g, p, cs, 1, 0, stream)
+                         : launch_tiles<false, 1>(mode, pal != nullptr, g, p, cs, 1, 0, stream);
+  return cuda_status(e);
+}
+
+}  // namespace
+
+extern "C" {
+
+fr_status julia_render(fr_complex c, fr_window win, int32_t width, int32_t height,
+                       int32_t max_iter, uint16_t* out_counts, fr_stream stream) {
+  return render_frame(false, c, win, width, height, max_iter, FR_FP32_FAST, fr_bands{0, 1, 0},
+                      out_counts, nullptr, nullptr, stream);
+}
+
+fr_status julia_render_ex(fr_complex c, fr_window win, int32_t width, int32_t height,
+                          int32_t max_iter, fr_mode mode, fr_bands bands, uint16_t* out_counts,
+                          const fr_palette* pal, uint8_t* out_rgba, fr_stream stream) {
+  return render_frame(false, c, win, width, height, max_iter, mode, bands, out_counts, pal,
+                      out_rgba, stream);
+}
+
+fr_status mandelbrot_param_map(fr_window win, int32_t width, int32_t height, int32_t max_iter,
+                               fr_mode mode, fr_bands bands, uint16_t* out_counts,
+                               const fr_palette* pal, uint8_t* out_rgba, fr_stream stream) {
+  return render_frame(true, fr_complex{0.0, 0.0}, win, width, height, max_iter, mode, bands,
+                      out_counts, pal, out_rgba, stream);
+}
+
+fr_status julia_render_path(const fr_complex* c_host, int32_t n_frames, fr_window win,
+                            int32_t width, int32_t height, int32_t max_iter, fr_mode mode,
+                            uint16_t* out_counts, const fr_palette* pal, uint8_t* out_rgba,
+                            fr_stream stream) {
+  if (n_frames < 0) return FR_ERR_INVALID_ARG;
+  fr_status st = check_frame(win, width, height, max_iter);
+  if (st != FR_OK) return st;
+  if (!mode_valid(mode)) return FR_ERR_UNSUPPORTED;
+  if (n_frames == 0) return FR_OK;
+  if (!c_host || !out_counts) return FR_ERR_INVALID_ARG;
+  if ((pal != nullptr) != (out_rgba != nullptr)) return FR_ERR_INVALID_ARG;
+  for (int32_t k = 0; k < n_frames; ++k)
+    if (!(is_fin(c_host[k].re) && is_fin(c_host[k].im))) return FR_ERR_INVALID_ARG;
+  fr::Palette p;
+  st = make_palette(pal, &p);
+  if (st != FR_OK) return st;
+  const fr::Geom g = make_geom(win, width, height, max_iter, fr_bands{0, 1, 0}, height,
+                               out_counts, out_rgba);
+  fr::CList<fr::kMaxPathChunk>* cs = new (std::nothrow) fr::CList<fr::kMaxPathChunk>;
+  if (!cs) return FR_ERR_CUDA;
+  cudaError_t e = cudaSuccess;
+  for (int32_t f0 = 0; f0 < n_frames && e == cudaSuccess; f0 += fr::kMaxPathChunk) {
+    const int nf = n_frames - f0 < fr::kMaxPathChunk ? n_frames - f0 : fr::kMaxPathChunk;
+    for (int k = 0; k < nf; ++k) cs->c[k] = make_double2(c_host[f0 + k].re, c_host[f0 + k].im);
+    e = launch_tiles<false, fr::kMaxPathChunk>(mode, pal != nullptr, g, p, *cs, nf, f0, stream);
+  }
+  delete cs;
+  return cuda_status(e);
+}
+
+fr_status colorize(const uint16_t* counts, int64_t n_pixels, int32_t max_iter,
+                   const fr_palette* pal, uint8_t* out_rgba, fr_stream stream) {
+  if (n_pixels < 0 || max_iter < 1) return FR_ERR_INVALID_ARG;
+  if (max_iter > 65535) return FR_ERR_UNSUPPORTED;
+  if (!pal) return FR_ERR_INVALID_ARG;
+  fr::Palette p;
+  fr_status st = make_palette(pal, &p);
+  if (st != FR_OK) return st;
+  if (n_pixels == 0) return FR_OK;
+  if (!counts || !out_rgba) return FR_ERR_INVALID_ARG;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool aligned = ((uintptr_t)counts % 16 == 0) && ((uintptr_t)out_rgba % 16 == 0);
+  const int64_t work = aligned ? (n_pixels >> 3) : n_pixels;
+  int64_t blocks = (work + fr::kThreads - 1) / fr::kThreads;
+  const int64_t cap = (int64_t)sms * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  uchar4* o = reinterpret_cast<uchar4*>(out_rgba);
+  if (aligned)
+    fr::colorize_kernel<<<(unsigned)blocks, fr::kThreads, 0, stream>>>(counts, n_pixels,
+                                                                        max_iter, p, o);
+  else
+    fr::colorize_scalar_kernel<<<(unsigned)blocks, fr::kThreads, 0, stream>>>(
+        counts, n_pixels, max_iter, p, o);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(cudaGetLastError());
+}
+
+int64_t fr_band_local_rows(int32_t height, fr_bands bands) {
+  if (height < 1) return -1;
+  return local_rows(height, bands);
+}
+
+int64_t fr_band_global_row(int32_t height, fr_bands b, int64_t local_row) {
+  const int64_t rows = fr_band_local_rows(height, b);
+  if (rows < 0 || local_row < 0 || local_row >= rows) return -1;
+  if (b.band_rows == 0) return local_row;
+  const int64_t band = local_row / b.band_rows;
+  const int64_t w = local_row - band * b.band_rows;
+  return (band * b.n_ranks + b.rank) * b.band_rows + w;
+}
+
+const char* fr_status_str(fr_status s) {
+  switch (s) {
+    case FR_OK: return "FR_OK";
+    case FR_ERR_INVALID_ARG: return "FR_ERR_INVALID_ARG: invalid argument";
+    case FR_ERR_TOO_LARGE: return "FR_ERR_TOO_LARGE: frame exceeds 2^31 pixels";
+    case FR_ERR_UNSUPPORTED: return "FR_ERR_UNSUPPORTED: unsupported mode or max_iter > 65535";
+    case FR_ERR_CUDA: return "FR_ERR_CUDA: CUDA launch or copy failed";
+  }
+  return "FR_ERR_UNKNOWN";
+}
+
+int32_t fr_last_cuda_error(void) { return g_last_cuda_error; }
+
+uint64_t fr_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char* fr_version(void) { return "libfractal 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,368 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+STRICT modes: bit-exact counts on every BASELINE config (full frames where the oracle
+finishes in seconds, sampled pixels at cfg4/cfg5 full size), fuzzed windows, ragged
+and degenerate sizes, bands and C-paths.  FAST modes: the DESIGN.md reading c-10
+tolerance -- the differing fraction is at most max(1e-4, 4 x the oracle's own 1-ulp
+sensitivity) and every differing pixel is certifiably within sqrt(2) pixels of the set
+boundary (distance estimate DE/2 <= sqrt(2) * pitch).
+"""
+import math
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1611_03079_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def fr():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1611_03079_b200 import binding
+    binding.load()
+    return binding
+
+
+def np16(t):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def sample16(t, py, px):
+    """t[py, px] for a uint16 CUDA tensor (indexed through an int16 view)."""
+    v = t.view(torch.int16)[torch.as_tensor(py, device=t.device), torch.as_tensor(px, device=t.device)]
+    return v.cpu().numpy().view(np.uint16)
+
+
+def strict(prec, fr):
+    return fr.Mode.FP32_STRICT if prec == 32 else fr.Mode.FP64_STRICT
+
+
+def fast(prec, fr):
+    return fr.Mode.FP32_FAST if prec == 32 else fr.Mode.FP64_FAST
+
+
+def gpu_julia(fr, c, win, w, h, mi, mode, bands=None, palette=None):
+    bands = bands or fr.FULL_FRAME
+    r = fr.julia_render_ex(c, win, w, h, mi, mode, bands, palette=palette)
+    torch.cuda.synchronize()
+    if palette is not None:
+        return np16(r[0]), r[1].cpu().numpy()
+    return np16(r)
+
+
+def gpu_mandel(fr, win, w, h, mi, mode, bands=None):
+    r = fr.mandelbrot_param_map(win, w, h, mi, mode, bands or fr.FULL_FRAME)
+    torch.cuda.synchronize()
+    return np16(r)
+
+
+def test_native_library_is_loaded(fr):
+    maps = open("/proc/self/maps").read()
+    assert "libfractal.so" in maps
+    assert "sm_100a" in fr.version()
+    assert torch.cuda.get_device_capability() == (10, 0)
+
+
+# ------------------------------------------------------------------ strict, full frames
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_strict_configs_full_frame(fr, name):
+    cfg = W.configs()[name]
+    win = cfg.window
+    ref = oracle.julia(cfg.c, win.center, win.half_w, win.half_h, cfg.width, cfg.height,
+                       cfg.max_iter, cfg.precision)
+    if cfg.colorize:
+        pal = W.palette("classic")
+        got, rgba = gpu_julia(fr, cfg.c, win, cfg.width, cfg.height, cfg.max_iter,
+                              strict(cfg.precision, fr), palette=pal)
+        np.testing.assert_array_equal(rgba, oracle.colorize(ref, cfg.max_iter, *pal))
+    else:
+        got = gpu_julia(fr, cfg.c, win, cfg.width, cfg.height, cfg.max_iter,
+                        strict(cfg.precision, fr))
+    np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+@pytest.mark.parametrize("c", list(W.FIG2_C) + list(W.FIG3_C))
+def test_strict_paper_parameters(fr, prec, c):
+    """Figure 2 and Figure 3 parameter values at 256^2."""
+    win = W.julia_window(256, 256)
+    ref = oracle.julia(c, win.center, win.half_w, win.half_h, 256, 256, 100, prec)
+    np.testing.assert_array_equal(gpu_julia(fr, c, win, 256, 256, 100, strict(prec, fr)), ref)
+
+
+@pytest.mark.parametrize("case", range(48))
+def test_strict_fuzz(fr, case):
+    c, win, w, h, mi = W.fuzz_cases(48, max_side=300)[case]
+    for prec in (32, 64):
+        ref = oracle.julia(c, win.center, win.half_w, win.half_h, w, h, mi, prec)
+        np.testing.assert_array_equal(gpu_julia(fr, c, win, w, h, mi, strict(prec, fr)), ref)
+        ref = oracle.mandelbrot(win.center, win.half_w, win.half_h, w, h, mi, prec)
+        np.testing.assert_array_equal(gpu_mandel(fr, win, w, h, mi, strict(prec, fr)), ref)
+
+
+@pytest.mark.parametrize("size", [(1, 1), (1, 37), (37, 1), (33, 9), (31, 7), (257, 129),
+                                  (8, 4), (32, 8), (65, 17)])
+@pytest.mark.parametrize("mi", [1, 2, 7, 100])
+def test_strict_ragged_and_degenerate(fr, size, mi):
+    w, h = size
+    c = W.FIG2_C[2]
+    win = W.julia_window(w, h, span_re=3.2)
+    for prec in (32, 64):
+        ref = oracle.julia(c, win.center, win.half_w, win.half_h, w, h, mi, prec)
+        np.testing.assert_array_equal(gpu_julia(fr, c, win, w, h, mi, strict(prec, fr)), ref)
+        ref = oracle.mandelbrot(-0.5 + 0j, 1.5, 1.5 * h / w, w, h, mi, prec)
+        got = gpu_mandel(fr, (-0.5 + 0j, 1.5, 1.5 * h / w), w, h, mi, strict(prec, fr))
+        np.testing.assert_array_equal(got, ref)
+
+
+def test_max_iter_65535(fr):
+    """The uint16 limit: interior pixels report 65535."""
+    win = W.julia_window(24, 16)
+    for prec in (32, 64):
+        ref = oracle.julia(-0.12 + 0.75j, win.center, win.half_w, win.half_h, 24, 16, 65535, prec)
+        assert (ref == 65535).any()
+        got = gpu_julia(fr, -0.12 + 0.75j, win, 24, 16, 65535, strict(prec, fr))
+        np.testing.assert_array_equal(got, ref)
+
+
+def test_every_pixel_written_once(fr):
+    """Sentinel-filled output: nothing left unwritten, nothing written outside."""
+    w, h = 333, 77
+    buf = torch.full((h * w + 64,), -1, dtype=torch.int16, device="cuda").view(torch.uint16)
+    out = buf[: h * w].view(h, w)
+    fr.julia_render_ex(0.285 + 0.01j, W.julia_window(w, h), w, h, 100, fr.Mode.FP32_STRICT,
+                       out=out)
+    torch.cuda.synchronize()
+    a = np16(buf)
+    assert (a[: h * w] != 0xFFFF).all()
+    assert (a[h * w:] == 0xFFFF).all()
+
+
+def test_largest_frame(fr):
+    """W*H = 2^31 (the S:182 limit): 64-bit offsets; corners and a sample match."""
+    w, h = 65536, 32768
+    out = torch.full((h, w), -1, dtype=torch.int16, device="cuda").view(torch.uint16)
+    win = W.julia_window(w, h)
+    fr.julia_render_ex(-0.8 + 0.156j, win, w, h, 3, fr.Mode.FP32_STRICT, out=out)
+    torch.cuda.synchronize()
+    assert not bool((out.view(torch.int16) == -1).any())
+    rng = np.random.default_rng(1)
+    px = np.r_[0, w - 1, 0, w - 1, rng.integers(0, w, 2000)]
+    py = np.r_[0, 0, h - 1, h - 1, rng.integers(0, h, 2000)]
+    ref = oracle.pixels("julia", -0.8 + 0.156j, win.center, win.half_w, win.half_h, w, h, 3, 32,
+                        px, py)
+    got = sample16(out, py, px)
+    np.testing.assert_array_equal(got, ref)
+    del out
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ paths (cfg4)
+def test_path_equals_single_frames(fr):
+    """julia_render_path(C[])[k] == julia_render_ex(C[k]) byte-exactly, across the
+    1024-frame launch chunk boundary, in fast and strict modes."""
+    cs = W.circle_path(1100)
+    w, h = 48, 27
+    win = W.julia_window(w, h)
+    for mode in (fr.Mode.FP32_FAST, fr.Mode.FP32_STRICT, fr.Mode.FP64_FAST):
+        pal = W.palette("fire")
+        frames, rgba = fr.julia_render_path(cs, win, w, h, 100, mode, palette=pal)
+        torch.cuda.synchronize()
+        frames = np16(frames)
+        rgba = rgba.cpu().numpy()
+        for k in (0, 1, 511, 1023, 1024, 1099):
+            one, one_rgba = gpu_julia(fr, complex(cs[k]), win, w, h, 100, mode, palette=pal)
+            np.testing.assert_array_equal(frames[k], one)
+            np.testing.assert_array_equal(rgba[k], one_rgba)
+
+
+def test_cfg4_strict_full_size_sampled_frames(fr):
+    """cfg4 at full size (4096 frames of 1080p in one call, 64-bit offsets): whole
+    frames at 8 path positions equal the oracle."""
+    cfg = W.configs()["cfg4"]
+    cs = W.circle_path(cfg.n_frames)
+    win = cfg.window
+    out = fr.julia_render_path(cs, win, cfg.width, cfg.height, cfg.max_iter, fr.Mode.FP32_STRICT)
+    torch.cuda.synchronize()
+    for k in (0, 1, 511, 1024, 2047, 2048, 3071, 4095):
+        ref = oracle.julia(complex(cs[k]), win.center, win.half_w, win.half_h, cfg.width,
+                           cfg.height, cfg.max_iter, 32)
+        np.testing.assert_array_equal(np16(out[k]), ref)
+    del out
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ Mandelbrot cfg5
+def test_cfg5_strict_full_size_sampled(fr):
+    """cfg5: 16384^2, max_iter 10000, fp64 deep zoom, full render on the GPU; 6000
+    random pixels plus one full row compared with the oracle."""
+    cfg = W.configs()["cfg5"]
+    win = cfg.window
+    got = fr.mandelbrot_param_map(win, cfg.width, cfg.height, cfg.max_iter, fr.Mode.FP64_STRICT)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(55)
+    px = np.r_[rng.integers(0, cfg.width, 6000), np.arange(0, cfg.width, 4)]
+    py = np.r_[rng.integers(0, cfg.height, 6000), np.full(cfg.width // 4, 8191)]
+    ref = oracle.pixels("mandelbrot", 0j, win.center, win.half_w, win.half_h, cfg.width,
+                        cfg.height, cfg.max_iter, 64, px, py)
+    np.testing.assert_array_equal(sample16(got, py, px), ref)
+    del got
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ bands
+@pytest.mark.parametrize("n_ranks", [2, 4, 8])
+def test_bands_equal_rows_of_full_render(fr, n_ranks):
+    w, h, br = 960, 547, 15
+    win = W.julia_window(w, h)
+    c = -0.7269 + 0.1889j
+    pal = W.palette("classic")
+    full, full_rgba = gpu_julia(fr, c, win, w, h, 1000, fr.Mode.FP32_FAST, palette=pal)
+    mfull = gpu_mandel(fr, (-0.6 + 0j, 1.6, 1.6 * h / w), w, h, 500, fr.Mode.FP64_STRICT)
+    rows_seen = []
+    for rank in range(n_ranks):
+        b = fr.Bands(br, n_ranks, rank)
+        rows = [fr.band_global_row(h, b, i) for i in range(fr.band_local_rows(h, b))]
+        rows_seen += rows
+        part, part_rgba = gpu_julia(fr, c, win, w, h, 1000, fr.Mode.FP32_FAST, bands=b,
+                                    palette=pal)
+        np.testing.assert_array_equal(part, full[rows])
+        np.testing.assert_array_equal(part_rgba, full_rgba[rows])
+        mpart = gpu_mandel(fr, (-0.6 + 0j, 1.6, 1.6 * h / w), w, h, 500, fr.Mode.FP64_STRICT,
+                           bands=b)
+        np.testing.assert_array_equal(mpart, mfull[rows])
+    assert sorted(rows_seen) == list(range(h))
+
+
+# ------------------------------------------------------------------ colour levels
+@pytest.mark.parametrize("n", [0, 1, 7, 8, 9, 1000, 12345, 1 << 20])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_colorize_standalone(fr, n, offset):
+    rng = np.random.default_rng(n + offset)
+    counts = rng.integers(0, 1001, size=n + offset).astype(np.uint16)
+    counts[::97] = 1000
+    t = torch.from_numpy(counts.view(np.int16)).cuda().view(torch.uint16)[offset:]
+    for name in ("classic", "fire"):
+        pal = W.palette(name)
+        got = fr.colorize(t, 1000, pal)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(got.cpu().numpy(), oracle.colorize(counts[offset:], 1000, *pal))
+    odd = (np.arange(7 * 4, dtype=np.uint8).reshape(7, 4), np.array([9, 8, 7, 6], np.uint8))
+    got = fr.colorize(t, 1000, odd)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), oracle.colorize(counts[offset:], 1000, *odd))
+
+
+def test_fused_colorize_matches_standalone(fr):
+    cfg = W.configs()["cfg2"]
+    pal = W.palette("fire")
+    counts, rgba = gpu_julia(fr, cfg.c, cfg.window, cfg.width, cfg.height, cfg.max_iter,
+                             fr.Mode.FP32_FAST, palette=pal)
+    t = torch.from_numpy(counts.view(np.int16)).cuda().view(torch.uint16)
+    again = fr.colorize(t, cfg.max_iter, pal)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(again.cpu().numpy(), rgba)
+
+
+# ------------------------------------------------------------------ fast-mode tolerance
+def _de_pass(kind, c, win, w, h, px, py):
+    """DE/2 <= sqrt(2) * pitch for every listed pixel (reading c-10)."""
+    pitch = 2.0 * max(win.half_w / w, win.half_h / h)
+    chunks = np.array_split(np.arange(px.size), max(1, min(64, px.size // 64)))
+    with ThreadPoolExecutor(max_workers=oracle.default_threads()) as ex:
+        parts = list(ex.map(lambda idx: oracle.distance_pixels(
+            kind, c, win.center, win.half_w, win.half_h, w, h, px[idx], py[idx]), chunks))
+    de = np.concatenate(parts) if parts else np.zeros(0)
+    worst = float((de / 2 / pitch).max()) if de.size else 0.0
+    return bool((de / 2 <= math.sqrt(2) * pitch).all()), worst
+
+
+def _sensitivity(kind, c, win, w, h, mi, prec, n=20000, seed=9):
+    rng = np.random.default_rng(seed)
+    px, py = rng.integers(0, w, n), rng.integers(0, h, n)
+    a = oracle.pixels(kind, c, win.center, win.half_w, win.half_h, w, h, mi, prec, px, py)
+    b = oracle.pixels_nudged(kind, c, win.center, win.half_w, win.half_h, w, h, mi, prec, px, py, 1)
+    return float((a != b).mean())
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_fast_mode_tolerance_julia(fr, name):
+    cfg = W.configs()[name]
+    win = cfg.window
+    ref = oracle.julia(cfg.c, win.center, win.half_w, win.half_h, cfg.width, cfg.height,
+                       cfg.max_iter, cfg.precision)
+    got = gpu_julia(fr, cfg.c, win, cfg.width, cfg.height, cfg.max_iter, fast(cfg.precision, fr))
+    diff = np.argwhere(got != ref)
+    frac = diff.shape[0] / ref.size
+    sens = _sensitivity("julia", cfg.c, win, cfg.width, cfg.height, cfg.max_iter, cfg.precision)
+    print(f"{name}: fast-vs-strict {frac:.3e}, 1-ulp sensitivity {sens:.3e}")
+    assert frac <= max(1e-4, 4 * sens)
+    if diff.size:
+        sel = diff if diff.shape[0] <= 20000 else diff[np.random.default_rng(0).choice(
+            diff.shape[0], 20000, replace=False)]
+        ok, worst = _de_pass("julia", cfg.c, win, cfg.width, cfg.height, sel[:, 1], sel[:, 0])
+        print(f"{name}: worst DE/2 = {worst:.3f} px")
+        assert ok
+
+
+def test_fast_mode_tolerance_cfg4_frames(fr):
+    cfg = W.configs()["cfg4"]
+    cs = W.circle_path(cfg.n_frames)
+    ks = [0, 700, 1365, 2047, 3000]
+    out = fr.julia_render_path(cs[ks], cfg.window, cfg.width, cfg.height, cfg.max_iter,
+                               fr.Mode.FP32_FAST)
+    torch.cuda.synchronize()
+    win = cfg.window
+    for i, k in enumerate(ks):
+        ref = oracle.julia(complex(cs[k]), win.center, win.half_w, win.half_h, cfg.width,
+                           cfg.height, cfg.max_iter, 32)
+        got = np16(out[i])
+        diff = np.argwhere(got != ref)
+        assert diff.shape[0] / ref.size <= 1e-4
+        if diff.size:
+            ok, _ = _de_pass("julia", complex(cs[k]), win, cfg.width, cfg.height, diff[:, 1],
+                             diff[:, 0])
+            assert ok
+
+
+def test_fast_mode_tolerance_cfg5_sampled(fr):
+    cfg = W.configs()["cfg5"]
+    win = cfg.window
+    got = fr.mandelbrot_param_map(win, cfg.width, cfg.height, cfg.max_iter, fr.Mode.FP64_FAST)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(77)
+    px, py = rng.integers(0, cfg.width, 3000), rng.integers(0, cfg.height, 3000)
+    ref = oracle.pixels("mandelbrot", 0j, win.center, win.half_w, win.half_h, cfg.width,
+                        cfg.height, cfg.max_iter, 64, px, py)
+    g = sample16(got, py, px)
+    bad = g != ref
+    sens = _sensitivity("mandelbrot", 0j, win, cfg.width, cfg.height, cfg.max_iter, 64, n=3000)
+    print(f"cfg5: fast-vs-strict {bad.mean():.3e}, 1-ulp sensitivity {sens:.3e}")
+    assert bad.mean() <= max(1e-4, 4 * sens)
+    if bad.any():
+        ok, worst = _de_pass("mandelbrot", 0j, win, cfg.width, cfg.height, px[bad], py[bad])
+        print(f"cfg5: worst DE/2 = {worst:.3f} px")
+        assert ok
+    del got
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ streams / launches
+def test_side_stream_and_launch_count(fr):
+    cfg = W.configs()["cfg1"]
+    before = fr.launch_count()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        a = fr.julia_render_ex(cfg.c, cfg.window, 64, 64, 100, fr.Mode.FP32_STRICT)
+    s.synchronize()
+    b = gpu_julia(fr, cfg.c, cfg.window, 64, 64, 100, fr.Mode.FP32_STRICT)
+    np.testing.assert_array_equal(np16(a), b)
+    assert fr.launch_count() == before + 2

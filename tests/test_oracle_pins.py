@@ -351,3 +351,43 @@ def test_fig2_parameters_lie_on_the_a39_cardioid(oracle_mod):
         ts.append(t)
     unwrapped = np.unwrap(ts)
     assert (np.diff(unwrapped) < 0).all()
+
+
+# ------------------------------------------------------------------ fast-mode tolerance tools
+def test_distance_estimate_closed_form_c_zero(oracle_mod):
+    """C = 0: Z_n = Z_0^(2^n), Z'_n = 2^n Z_0^(2^n - 1), so DE = |Z_0| ln|Z_0| exactly for
+    every n; the true distance to K = unit disc is |Z_0| - 1 >= DE/2 (Koebe)."""
+    for r, th in [(1.5, 0.3), (1.01, 2.0), (3.0, -1.0), (1.0001, 0.7)]:
+        z0 = r * complex(math.cos(th), math.sin(th))
+        de = oracle.distance_estimate("julia", z0, 0j)
+        assert de == pytest.approx(r * math.log(r), rel=1e-9)
+        assert de / 2 <= r - 1 + 1e-15
+    assert oracle.distance_estimate("julia", 0.5 + 0j, 0j) == 0.0  # inside: never escapes
+
+
+def test_distance_estimate_mandelbrot_real_axis(oracle_mod):
+    """For real c > 1/4 the nearest point of M lies on the main-cardioid border
+    e^{it}/2 - e^{2it}/4 (the rightmost part of M), so that distance d must satisfy the
+    Koebe-type bounds DE/2 <= d <= 2 DE."""
+    t = np.linspace(-math.pi, math.pi, 400001)
+    border = np.exp(1j * t) / 2 - np.exp(2j * t) / 4
+    for c in (0.3, 0.5, 1.0, 2.5):
+        de = oracle.distance_estimate("mandelbrot", 0j, complex(c, 0))
+        d = np.abs(border - c).min()
+        assert de / 2 <= d <= 2 * de
+    assert oracle.distance_estimate("mandelbrot", 0j, -1 + 0j, 10000) == 0.0
+
+
+def test_nudged_pixels(oracle_mod):
+    """nudge = 0 reproduces the sampled strict counts exactly; a 1-ulp nudge of Z_0
+    changes some, but few, counts at max_iter 1000 (the problem's own sensitivity)."""
+    rng = np.random.default_rng(5)
+    px, py = rng.integers(0, 640, 4000), rng.integers(0, 360, 4000)
+    args = ("julia", -0.7269 + 0.1889j, 0j, 2.0, 1.125, 640, 360, 1000)
+    for prec in PRECS:
+        a = oracle.pixels(*args, prec, px, py)
+        np.testing.assert_array_equal(a, oracle.pixels_nudged(*args, prec, px, py, 0))
+        c = oracle.pixels_nudged(*args, prec, px, py, 1)
+        assert (a != c).sum() < 0.1 * a.size
+        if prec == 32:
+            assert (a != c).sum() > 0
