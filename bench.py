@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""Benchmark of the escape-time hot path (arXiv 1611.03079) on 1..8 B200s.
+
+Workload (BASELINE.json configs[3], weak-scaled): the C-path sweep of 1080p Julia
+frames (1920x1080, max_iter 100, FP32 fast mode) with C on |C| = 0.7885.  At N GPUs
+the path has F = 512*N frames, th_k = 2 pi k / F, and frame k is rendered by rank
+k mod N (cyclic frames, no data-path collective); every rank renders 512 frames per
+step, so at N = 8 one step is exactly configs[3] (4096 frames).  A step = one pass of
+the whole hot path over the rank's batch: parameter derivation, region-covering map,
+escape-time iteration, uint16 count store, frame loop (one julia_render_path call).
+
+Metric: Gpixel-iter/s = sum of escape counts / time (BASELINE.json metric), whole job;
+1080p frames/s is reported beside it.  Prints ONE JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+FRAMES_PER_RANK = 512
+W_PX, H_PX, MAX_ITER = 1920, 1080, 100
+RADIUS = 0.7885
+SM_COUNT, FP32_LANES_PER_SM, FP64_LANES_PER_SM = 148, 128, 64
+INSTR_PER_ITER = 6  # issue slots per pixel-iteration at the roofline
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def path_for(world: int, rank: int):
+    from paper_1611_03079_b200 import workloads as W
+    full = W.circle_path(FRAMES_PER_RANK * world, RADIUS)
+    return full[rank::world]
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- CPU oracle
+def cpu_oracle_rate(cs, seconds: float = 12.0, threads: int | None = None):
+    """The oracle as it stands (strict, plain C, all host cores) on a bounded sample of
+    the same workload: whole frames of the rank's path until ~`seconds` elapse."""
+    import oracle
+    from paper_1611_03079_b200 import workloads as W
+    win = W.julia_window(W_PX, H_PX)
+    threads = threads or oracle.default_threads()
+    order = np.random.default_rng(0).permutation(len(cs))
+    total, frames, t0 = 0, 0, time.perf_counter()
+    for k in order:
+        g = oracle.julia(complex(cs[k]), win.center, win.half_w, win.half_h, W_PX, H_PX,
+                         MAX_ITER, 32, threads)
+        total += int(g.sum(dtype=np.int64))
+        frames += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": total / dt / 1e9, "unit": "Gpixel-iter/s", "cores": threads,
+            "kind": "oracle", "frames_per_s": frames / dt,
+            "sample": f"{frames} of the {len(cs)} rank-0 1080p frames (random order), strict "
+                      f"fp32 scalar C oracle, {threads} threads, {dt:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_1611_03079_b200 import workloads as W
+    cs = path_for(world, 0)
+    win = W.julia_window(W_PX, H_PX)
+    threads = oracle.default_threads()
+    per_step = 2  # frames of the rank-0 batch per step (bounded sample)
+    order = np.random.default_rng(0).permutation(len(cs))
+
+    def step(i):
+        s = 0
+        for j in range(per_step):
+            k = order[(i * per_step + j) % len(order)]
+            g = oracle.julia(complex(cs[k]), win.center, win.half_w, win.half_h, W_PX, H_PX,
+                             MAX_ITER, 32, threads)
+            s += int(g.sum(dtype=np.int64))
+        return s
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    total = 0
+    for i in range(args.steps):
+        total += step(args.warmup + i)
+    dt = time.perf_counter() - t0
+    v = total / dt / 1e9
+    line = {
+        "impl": "reference", "metric": "Gpixel-iter/s", "value": v, "unit": "Gpixel-iter/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "cfg4 C-path, 1080p, max_iter 100 (bounded sample)",
+                   "frames_per_step": per_step, "width": W_PX, "height": H_PX,
+                   "max_iter": MAX_ITER},
+        "cpu_baseline": {"value": v, "unit": "Gpixel-iter/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{per_step} random frames of the rank-0 batch per step, "
+                                   f"strict fp32 scalar C oracle on {threads} threads"},
+        "e2e": {"value": v, "unit": "Gpixel-iter/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extra", action="store_true", help="skip the per-config extras")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1611_03079_b200 import binding as fr
+    from paper_1611_03079_b200 import workloads as W
+
+    fr.load()
+    win = W.julia_window(W_PX, H_PX)
+    cs = path_for(world, rank)
+    nf = len(cs)
+    out = torch.empty((nf, H_PX, W_PX), dtype=torch.uint16, device="cuda")
+    stream = torch.cuda.current_stream()
+    mode = fr.Mode.FP32_FAST
+
+    def step():
+        fr.julia_render_path(cs, win, W_PX, H_PX, MAX_ITER, mode, out=out, stream=stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    iters_per_step = int((out.view(torch.int16).to(torch.int64) & 0xFFFF).sum().item())
+    barrier()
+
+    # ---- timed region: K steps, per-launch CUDA events on the launching stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    l0 = fr.launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        t_end.record(stream)
+        barrier()
+    launches = fr.launch_count() - l0
+    elapsed_ms = t_start.elapsed_time(t_end)
+    kernel_ms = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    clocks = clk.summary()
+
+    total_iters = iters_per_step * args.steps
+    tot = torch.tensor([float(total_iters)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    job_iters = float(tot.item())
+    value = job_iters / (elapsed_ms * 1e-3) / 1e9
+    frames_per_s = nf * world * args.steps / (elapsed_ms * 1e-3)
+
+    # ---- roofline of the dominant (only) kernel: escape_tile_kernel
+    peaks = measured_peaks()
+    f_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_gpix = SM_COUNT * FP32_LANES_PER_SM * f_max * 1e6 / INSTR_PER_ITER / 1e9
+    kavg = statistics.mean(kernel_ms)
+    achieved = iters_per_step / (kavg * 1e-3) / 1e9
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak_gpix, "unit": "Gpixel-iter/s",
+            "frac": achieved / peak_gpix, "traffic": None,
+            "kernel": "fr::escape_tile_kernel<float,fast,julia,path>",
+            "peak_basis": f"{SM_COUNT} SMs x {FP32_LANES_PER_SM} FP32 lanes x {f_max:.0f} MHz "
+                          f"(MEASURED_PEAKS.json sm_max_mhz) / {INSTR_PER_ITER} issue slots per "
+                          "pixel-iteration",
+            "kernel_ms_avg": kavg}
+    if clocks.get("sm_mhz"):
+        roof["frac_at_measured_clock"] = achieved / (peak_gpix * clocks["sm_mhz"] / f_max)
+    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(traffic_file):
+        try:
+            roof["traffic"] = json.load(open(traffic_file)).get("bench_kernel_dram_bytes")
+        except Exception:
+            pass
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": "Gpixel-iter/s", "value": value, "unit": "Gpixel-iter/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "cfg4 C-path sweep (BASELINE configs[3]), weak-scaled: "
+                                   f"{FRAMES_PER_RANK} frames/GPU, F={FRAMES_PER_RANK}*N frames "
+                                   "on |C|=0.7885, frame k -> rank k mod N",
+                       "width": W_PX, "height": H_PX, "max_iter": MAX_ITER, "mode": "FP32_FAST",
+                       "frames_per_step": nf * world, "parallelism": f"frames{world}",
+                       "l2": f"output {nf * W_PX * H_PX * 2 / 1e9:.2f} GB per step per GPU "
+                             "(> 126 MB L2), no L2 reuse between steps"},
+            "frames_per_s": frames_per_s,
+            "pixel_iters_per_step": job_iters / args.steps,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "roofline": roof,
+        }
+    # ---- end-to-end through the public API with HOST buffers (pinned), N GPUs
+    e2e = measure_e2e(fr, W, cs, win, world, args, barrier, stream)
+    if rank == 0:
+        line["e2e"] = e2e
+        if world == 1:
+            line["cpu_baseline"] = cpu_oracle_rate(cs, seconds=args.cpu_seconds)
+            if not args.no_extra:
+                line["configs"] = extras(fr, W, torch)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_e2e(fr, W, cs, win, world, args, barrier, stream):
+    """Same metric end to end: per step the C values go host->device (kernel params from
+    the host array), the frames are rendered in chunks and every chunk's counts are
+    copied device->host into pinned memory on a second stream, overlapped with the next
+    chunk's rendering."""
+    import torch
+    import torch.distributed as dist
+    nf = len(cs)
+    chunk = 64
+    host = torch.empty((nf, H_PX, W_PX), dtype=torch.int16, pin_memory=True)
+    dev = [torch.empty((chunk, H_PX, W_PX), dtype=torch.uint16, device="cuda") for _ in range(2)]
+    copy_stream = torch.cuda.Stream()
+    done = [torch.cuda.Event() for _ in range(2)]
+    rendered = [torch.cuda.Event() for _ in range(2)]
+
+    def step():
+        for j, f0 in enumerate(range(0, nf, chunk)):
+            b = j % 2
+            stream.wait_event(done[b])
+            n = min(chunk, nf - f0)
+            fr.julia_render_path(cs[f0:f0 + n], win, W_PX, H_PX, MAX_ITER, fr.Mode.FP32_FAST,
+                                 out=dev[b], stream=stream)
+            rendered[b].record(stream)
+            copy_stream.wait_event(rendered[b])
+            with torch.cuda.stream(copy_stream):
+                host[f0:f0 + n].copy_(dev[b][:n].view(torch.int16), non_blocking=True)
+            done[b].record(copy_stream)
+        stream.wait_stream(copy_stream)
+
+    steps = max(2, min(args.steps, 5))
+    for _ in range(2):
+        step()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        step()
+    t1.record(stream)
+    barrier()
+    ms = t0.elapsed_time(t1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    iters = int(host.numpy().view(np.uint16).sum(dtype=np.int64))
+    tot = torch.tensor([float(iters)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    return {"value": float(tot.item()) * steps / (ms * 1e-3) / 1e9, "unit": "Gpixel-iter/s",
+            "h2d_bytes_per_step": int(nf * 16), "d2h_bytes_per_step": int(nf * H_PX * W_PX * 2),
+            "steps": steps, "ms_per_step": ms / steps,
+            "note": "C values (16 B/frame) host->device as kernel parameters; uint16 counts "
+                    "device->host into pinned memory, chunked (64 frames) and overlapped"}
+
+
+def extras(fr, W, torch):
+    """Per-config single-GPU figures (fast mode) for the other BASELINE configs."""
+    res = {}
+    peaks = measured_peaks()
+    f_max = float(peaks.get("sm_max_mhz", 1965.0))
+    for name in ("cfg2", "cfg3", "cfg5"):
+        cfg = W.configs()[name]
+        prec = cfg.precision
+        pal = W.palette("classic") if cfg.colorize else None
+        out = torch.empty((cfg.height, cfg.width), dtype=torch.uint16, device="cuda")
+        rgba = (torch.empty((cfg.height, cfg.width, 4), dtype=torch.uint8, device="cuda")
+                if pal else None)
+        if cfg.kind == "julia":
+            mode = fr.Mode.FP32_FAST
+
+            def fn():
+                fr.julia_render_ex(cfg.c, cfg.window, cfg.width, cfg.height, cfg.max_iter, mode,
+                                   out=out, palette=pal, out_rgba=rgba)
+        else:
+            mode = fr.Mode.FP64_FAST
+
+            def fn():
+                fr.mandelbrot_param_map(cfg.window, cfg.width, cfg.height, cfg.max_iter, mode,
+                                        out=out)
+        reps = 2 if name == "cfg5" else 50
+        fn()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        b.synchronize()
+        ms = a.elapsed_time(b) / reps
+        s = int((out.view(torch.int16).to(torch.int64) & 0xFFFF).sum().item())
+        lanes = FP64_LANES_PER_SM if prec == 64 else FP32_LANES_PER_SM
+        peak = SM_COUNT * lanes * f_max * 1e6 / INSTR_PER_ITER / 1e9
+        res[name] = {"ms": ms, "gpix_iter_s": s / (ms * 1e-3) / 1e9, "pixel_iters": s,
+                     "frac_of_alu_peak": s / (ms * 1e-3) / 1e9 / peak, "mode": mode.name,
+                     "fused_colorize": bool(pal), "reps": reps,
+                     "note": "back-to-back launches, CUDA events"}
+        del out, rgba
+    torch.cuda.empty_cache()
+    return res
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -75,7 +75,7 @@ def _load():
                                                i64, ctypes.c_long, vp]
         lib.oracle_distance_pixels.restype = i32
         lib.oracle_pixels_nudged.argtypes = [i32, f64, f64, f64, f64, f64, f64, i64, i64, i32, i32,
-                                             vp, vp, i64, i32, vp]
+                                             vp, vp, i64, i32, vp, i32]
         lib.oracle_pixels_nudged.restype = i32
         _lib = lib
         return lib
@@ -215,7 +215,7 @@ def distance_pixels(kind: str, c: complex, center: complex, half_w: float, half_
 
 def pixels_nudged(kind: str, c: complex, center: complex, half_w: float, half_h: float,
                   width: int, height: int, max_iter: int, precision, px, py,
-                  nudge: int = 1) -> np.ndarray:
+                  nudge: int = 1, threads: int | None = None) -> np.ndarray:
     """Strict counts with the start value's real part moved by `nudge` ulps."""
     px = np.ascontiguousarray(px, dtype=np.int64)
     py = np.ascontiguousarray(py, dtype=np.int64)
@@ -223,7 +223,8 @@ def pixels_nudged(kind: str, c: complex, center: complex, half_w: float, half_h:
     m = {"julia": 0, "mandelbrot": 1}[kind]
     rc = _load().oracle_pixels_nudged(m, c.real, c.imag, center.real, center.imag, half_w, half_h,
                                       width, height, max_iter, _prec(precision), _ptr(px),
-                                      _ptr(py), px.size, nudge, _ptr(out))
+                                      _ptr(py), px.size, nudge, _ptr(out),
+                                      threads or default_threads())
     if rc != 0:
         raise ValueError("oracle_pixels_nudged: invalid arguments")
     return out

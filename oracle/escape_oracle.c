@@ -115,17 +115,28 @@ int oracle_escape_f64(double zre, double zim, double cre, double cim, int max_it
 /* One pixel of a Julia frame (Z_0 from the pixel, fixed C) or of a
  * Mandelbrot parameter map (C from the pixel, Z_0 = 0).  precision is
  * 32 or 64; for 32 the double inputs are rounded to binary32 once (c-8). */
-static int pixel_count(int mandel, int precision, double c_re, double c_im, double center_re,
-                       double center_im, double half_w, double half_h, int64_t width,
-                       int64_t height, int64_t px, int64_t py, int max_iter) {
+static int pixel_count_n(int mandel, int precision, double c_re, double c_im,
+                         double center_re, double center_im, double half_w, double half_h,
+                         int64_t width, int64_t height, int64_t px, int64_t py, int max_iter,
+                         int nudge) {
     double re = oracle_pixel_re(center_re, half_w, width, px);
     double im = oracle_pixel_im(center_im, half_h, height, py);
     if (precision == 32) {
-        if (mandel) return oracle_escape_f32(0.0f, 0.0f, (float)re, (float)im, max_iter);
-        return oracle_escape_f32((float)re, (float)im, (float)c_re, (float)c_im, max_iter);
+        float r = (float)re;
+        for (int k = 0; k < nudge; ++k) r = nextafterf(r, INFINITY);
+        if (mandel) return oracle_escape_f32(0.0f, 0.0f, r, (float)im, max_iter);
+        return oracle_escape_f32(r, (float)im, (float)c_re, (float)c_im, max_iter);
     }
+    for (int k = 0; k < nudge; ++k) re = nextafter(re, INFINITY);
     if (mandel) return oracle_escape_f64(0.0, 0.0, re, im, max_iter);
     return oracle_escape_f64(re, im, c_re, c_im, max_iter);
+}
+
+static int pixel_count(int mandel, int precision, double c_re, double c_im, double center_re,
+                       double center_im, double half_w, double half_h, int64_t width,
+                       int64_t height, int64_t px, int64_t py, int max_iter) {
+    return pixel_count_n(mandel, precision, c_re, c_im, center_re, center_im, half_w, half_h,
+                         width, height, px, py, max_iter, 0);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -144,6 +155,7 @@ typedef struct {
     const int64_t* py;
     int64_t n_pix;
     int64_t next; /* shared work counter */
+    int nudge;    /* ulps added to the start value's real part (0 = none) */
 } job_t;
 
 static void* grid_worker(void* arg) {
@@ -167,10 +179,10 @@ static void* list_worker(void* arg) {
         if (i0 >= j->n_pix) break;
         int64_t i1 = i0 + chunk < j->n_pix ? i0 + chunk : j->n_pix;
         for (int64_t i = i0; i < i1; ++i)
-            j->out[i] = (uint16_t)pixel_count(j->mandel, j->precision, j->c_re, j->c_im,
-                                              j->center_re, j->center_im, j->half_w,
-                                              j->half_h, j->width, j->height, j->px[i],
-                                              j->py[i], j->max_iter);
+            j->out[i] = (uint16_t)pixel_count_n(j->mandel, j->precision, j->c_re, j->c_im,
+                                                j->center_re, j->center_im, j->half_w,
+                                                j->half_h, j->width, j->height, j->px[i],
+                                                j->py[i], j->max_iter, j->nudge);
     }
     return NULL;
 }
@@ -202,7 +214,7 @@ int oracle_julia(double c_re, double c_im, double center_re, double center_im, d
                  uint16_t* out, int threads) {
     if (!args_ok(precision, width, height, max_iter) || !out) return -1;
     job_t j = {0, precision, max_iter, c_re, c_im, center_re, center_im, half_w, half_h,
-               width, height, out, NULL, NULL, 0, 0};
+               width, height, out, NULL, NULL, 0, 0, 0};
     return run_threads(&j, threads, grid_worker);
 }
 
@@ -213,7 +225,7 @@ int oracle_mandel(double center_re, double center_im, double half_w, double half
                   int threads) {
     if (!args_ok(precision, width, height, max_iter) || !out) return -1;
     job_t j = {1, precision, max_iter, 0.0, 0.0, center_re, center_im, half_w, half_h,
-               width, height, out, NULL, NULL, 0, 0};
+               width, height, out, NULL, NULL, 0, 0, 0};
     return run_threads(&j, threads, grid_worker);
 }
 
@@ -230,7 +242,25 @@ int oracle_pixels(int mandel, double c_re, double c_im, double center_re, double
     for (int64_t i = 0; i < n_pix; ++i)
         if (px[i] < 0 || px[i] >= width || py[i] < 0 || py[i] >= height) return -1;
     job_t j = {mandel ? 1 : 0, precision, max_iter, c_re, c_im, center_re, center_im, half_w,
-               half_h, width, height, out, px, py, n_pix, 0};
+               half_h, width, height, out, px, py, n_pix, 0, 0};
+    return run_threads(&j, threads, list_worker);
+}
+
+/* As oracle_pixels, with the start value's real part (Julia Z_0, Mandelbrot C) moved by
+ * `nudge` ulps of the working precision toward +inf: the problem's own 1-ulp
+ * sensitivity, against which fast-mode differences are judged (reading c-10). */
+int oracle_pixels_nudged(int mandel, double c_re, double c_im, double center_re,
+                         double center_im, double half_w, double half_h, int64_t width,
+                         int64_t height, int max_iter, int precision, const int64_t* px,
+                         const int64_t* py, int64_t n_pix, int nudge, uint16_t* out,
+                         int threads) {
+    if (!args_ok(precision, width, height, max_iter) || n_pix < 0 || nudge < 0) return -1;
+    if (n_pix == 0) return 0;
+    if (!px || !py || !out) return -1;
+    for (int64_t i = 0; i < n_pix; ++i)
+        if (px[i] < 0 || px[i] >= width || py[i] < 0 || py[i] >= height) return -1;
+    job_t j = {mandel ? 1 : 0, precision, max_iter, c_re, c_im, center_re, center_im, half_w,
+               half_h, width, height, out, px, py, n_pix, 0, nudge};
     return run_threads(&j, threads, list_worker);
 }
 
@@ -313,34 +343,6 @@ int oracle_distance_pixels(int mandel, double c_re, double c_im, double center_r
         double im = oracle_pixel_im(center_im, half_h, height, py[i]);
         out[i] = mandel ? oracle_distance_estimate(1, 0.0, 0.0, re, im, max_iter)
                         : oracle_distance_estimate(0, re, im, c_re, c_im, max_iter);
-    }
-    return 0;
-}
-
-/* Strict counts at selected pixels with the pixel's start value (Julia Z_0, or the
- * Mandelbrot C) real part moved by `nudge` ulps of the working precision: the
- * problem's own 1-ulp sensitivity, against which fast-mode differences are judged. */
-int oracle_pixels_nudged(int mandel, double c_re, double c_im, double center_re,
-                         double center_im, double half_w, double half_h, int64_t width,
-                         int64_t height, int max_iter, int precision, const int64_t* px,
-                         const int64_t* py, int64_t n_pix, int nudge, uint16_t* out) {
-    if (!args_ok(precision, width, height, max_iter) || n_pix < 0) return -1;
-    for (int64_t i = 0; i < n_pix; ++i) {
-        if (px[i] < 0 || px[i] >= width || py[i] < 0 || py[i] >= height) return -1;
-        double re = oracle_pixel_re(center_re, half_w, width, px[i]);
-        double im = oracle_pixel_im(center_im, half_h, height, py[i]);
-        if (precision == 32) {
-            float r = (float)re;
-            for (int k = 0; k < nudge; ++k) r = nextafterf(r, INFINITY);
-            out[i] = (uint16_t)(mandel ? oracle_escape_f32(0.0f, 0.0f, r, (float)im, max_iter)
-                                       : oracle_escape_f32(r, (float)im, (float)c_re,
-                                                           (float)c_im, max_iter));
-        } else {
-            double r = re;
-            for (int k = 0; k < nudge; ++k) r = nextafter(r, INFINITY);
-            out[i] = (uint16_t)(mandel ? oracle_escape_f64(0.0, 0.0, r, im, max_iter)
-                                       : oracle_escape_f64(r, im, c_re, c_im, max_iter));
-        }
     }
     return 0;
 }

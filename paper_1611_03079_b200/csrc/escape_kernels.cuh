@@ -192,70 +192,225 @@ __device__ __forceinline__ uchar4 colour_of(const uchar4* spal, const Palette& p
 }
 
 // ----------------------------------------------------------------------------------
-// Static-tile kernel: one pixel per thread, 8x4 warp tiles, iteration in unrolled
-// blocks of K with a warp-vote (__any_sync) exit.  blockIdx.x = tile, blockIdx.y =
-// frame of the path chunk (C = cs.c[blockIdx.y]); MANDEL takes C from the pixel and
-// Z_0 = 0.
+// Static-tile kernel (S): one pixel per thread, 8x4 warp tiles in a 32x8 CTA tile.  The
+// CTA computes its tile's axis values once (32 re + 8 im, binary64 -> state type) into
+// shared memory and then renders a GROUP of frames of the path chunk for that tile
+// (frames [blockIdx.y * fpc, ...)), so the per-pixel map cost is amortised over the
+// group.  Iteration runs in unrolled blocks of K with a warp-vote (__any_sync) exit; the
+// count is exact per iteration (sticky alive predicate + predicated increment).
+// MANDEL takes C from the pixel and Z_0 = 0.
 // ----------------------------------------------------------------------------------
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int NC>
 __global__ void __launch_bounds__(kThreads)
-escape_tile_kernel(const Geom g, const Palette pal, const CList<NC> cs, int frame0) {
+escape_tile_kernel(const Geom g, const Palette pal, const CList<NC> cs, int frame0,
+                   int n_frames, int fpc) {
   __shared__ uchar4 spal[COLOR ? 256 : 1];
+  __shared__ T sre[kTileW];
+  __shared__ T sim[kTileH];
+  const int tile = blockIdx.x;
+  const int ty = tile / g.tiles_x;
+  const int tx = tile - ty * g.tiles_x;
+  {
+    const int t = threadIdx.x;
+    if (t < kTileW) {
+      const int px = min(tx * kTileW + t, g.W - 1);
+      sre[t] = to_state<T, STRICT>(pixel_re(g, px));
+    } else if (t < kTileW + kTileH) {
+      const int ly = min(ty * kTileH + (t - kTileW), g.rows - 1);
+      sim[t - kTileW] = to_state<T, STRICT>(pixel_im(g, global_row(g, ly)));
+    }
+    if (COLOR) spal[t] = pal.e[t];
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int cx = (warp & 3) * kWarpW + (lane & 7);
+  const int cy = (warp >> 2) * kWarpH + (lane >> 3);
+  const int px = tx * kTileW + cx;
+  const int ly = ty * kTileH + cy;
+  const bool inside = (px < g.W) && (ly < g.rows);
+  const T are = sre[cx];
+  const T aim = sim[cy];
+  const int max_iter = g.max_iter;
+  const int f0 = blockIdx.y * fpc;
+  const int f1 = min(f0 + fpc, n_frames);
+  const int64_t pix_off = (int64_t)ly * g.W + px;
+
+  for (int f = f0; f < f1; ++f) {
+    T x, y, cr, ci;
+    if (MANDEL) {
+      x = T(0);
+      y = T(0);
+      cr = are;
+      ci = aim;
+    } else {
+      x = are;
+      y = aim;
+      const double2 c = cs.c[NC == 1 ? 0 : f];
+      cr = to_state<T, STRICT>(c.x);
+      ci = to_state<T, STRICT>(c.y);
+    }
+    unsigned alive = inside ? 1u : 0u;
+    int cnt = 0;
+    int n = 0;
+    bool more = true;
+    while (n + K <= max_iter) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
+      n += K;
+      if (!__any_sync(kFull, alive)) {
+        more = false;
+        break;
+      }
+    }
+    if (more) {
+      for (; n < max_iter; ++n) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
+    }
+    if (inside) {
+      const int count = cnt < max_iter ? cnt : max_iter;
+      const int64_t off = (int64_t)(frame0 + f) * g.frame_stride + pix_off;
+      g.counts[off] = (uint16_t)count;
+      if (COLOR) g.rgba[off] = colour_of(spal, pal, count, max_iter);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------------
+// Persistent lane-refill kernel (R) for one frame with a heavy-tailed count
+// distribution (SURVEY §7 hard part 1).  Each warp owns a 32x8-pixel chunk at a time,
+// taken from a global atomic chunk counter (self-resetting workspace).  Every lane
+// iterates its own pixel in blocks of K (exact per-iteration count); when at least TH
+// lanes have finished, the finished lanes store their count (and colour) and take the
+// next pixels of the chunk (prefix rank over the finished lanes), grabbing a new chunk
+// when it is exhausted.  SIMT lanes therefore stay busy whatever the neighbours' counts.
+// ----------------------------------------------------------------------------------
+struct Workspace {
+  unsigned int next_chunk;
+  unsigned int done_ctas;
+  unsigned int pad[30];
+};
+
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH>
+__global__ void __launch_bounds__(kThreads)
+escape_refill_kernel(const Geom g, const Palette pal, const double2 c, Workspace* ws,
+                     unsigned n_chunks) {
+  __shared__ uchar4 spal[COLOR ? 256 : 1];
+  __shared__ T tre[kThreads / 32][kTileW];
+  __shared__ T tim[kThreads / 32][kTileH];
   if (COLOR) {
     spal[threadIdx.x] = pal.e[threadIdx.x];
     __syncthreads();
   }
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int tile = blockIdx.x;
-  const int ty = tile / g.tiles_x;
-  const int tx = tile - ty * g.tiles_x;
-  const int px = tx * kTileW + (warp & 3) * kWarpW + (lane & 7);
-  const int ly = ty * kTileH + (warp >> 2) * kWarpH + (lane >> 3);
-  const bool inside = (px < g.W) && (ly < g.rows);
-  const int f = blockIdx.y;
-
-  T x, y, cr, ci;
-  {
-    const int gy = global_row(g, inside ? ly : 0);
-    const double re = pixel_re(g, inside ? px : 0);
-    const double im = pixel_im(g, gy);
-    if (MANDEL) {
-      x = T(0);
-      y = T(0);
-      cr = to_state<T, STRICT>(re);
-      ci = to_state<T, STRICT>(im);
-    } else {
-      x = to_state<T, STRICT>(re);
-      y = to_state<T, STRICT>(im);
-      const double2 c = cs.c[NC == 1 ? 0 : f];
-      cr = to_state<T, STRICT>(c.x);
-      ci = to_state<T, STRICT>(c.y);
-    }
-  }
-
-  unsigned alive = inside ? 1u : 0u;
-  int cnt = 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
   const int max_iter = g.max_iter;
-  int n = 0;
-  bool more = true;
-  while (n + K <= max_iter) {
+  T jcr = T(0), jci = T(0);
+  if (!MANDEL) {
+    jcr = to_state<T, STRICT>(c.x);
+    jci = to_state<T, STRICT>(c.y);
+  }
+
+  // warp-uniform chunk state
+  int chunk_x0 = 0, chunk_y0 = 0;  // pixel origin of the current chunk
+  int next_idx = kTileW * kTileH;  // next undispensed pixel of the chunk (256 = exhausted)
+  bool exhausted = false;          // no more chunks
+
+  // per-lane pixel state
+  T x = T(0), y = T(0), cr = jcr, ci = jci;
+  unsigned alive = 0u;
+  int cnt = 0;
+  int gx = -1, ly = -1;  // gx < 0: lane holds no pixel
+
+  for (;;) {
+    // ---- assignment: free lanes take the next pixels of the chunk (prefix rank)
+    for (;;) {
+      const unsigned free_mask = __ballot_sync(kFull, gx < 0);
+      if (free_mask == 0u || exhausted) break;
+      if (next_idx >= kTileW * kTileH) {
+        unsigned cid = 0;
+        if (lane == 0) cid = atomicAdd(&ws->next_chunk, 1u);
+        cid = __shfl_sync(kFull, cid, 0);
+        if (cid >= n_chunks) {
+          exhausted = true;
+          break;
+        }
+        const int cty = (int)(cid / (unsigned)g.tiles_x);
+        const int ctx = (int)cid - cty * g.tiles_x;
+        chunk_x0 = ctx * kTileW;
+        chunk_y0 = cty * kTileH;
+        __syncwarp();
+        tre[warp][lane] = to_state<T, STRICT>(pixel_re(g, min(chunk_x0 + lane, g.W - 1)));
+        if (lane < kTileH)
+          tim[warp][lane] = to_state<T, STRICT>(
+              pixel_im(g, global_row(g, min(chunk_y0 + lane, g.rows - 1))));
+        __syncwarp();
+        next_idx = 0;
+      }
+      const int avail = kTileW * kTileH - next_idx;
+      const int nfree = __popc(free_mask);
+      const int take = nfree < avail ? nfree : avail;
+      const int rank = __popc(free_mask & lt_mask);
+      if (((free_mask >> lane) & 1u) && rank < take) {
+        const int idx = next_idx + rank;
+        const int lx = idx & (kTileW - 1);
+        const int lyy = idx >> 5;
+        const int px = chunk_x0 + lx;
+        const int row = chunk_y0 + lyy;
+        if (px < g.W && row < g.rows) {  // else: off-frame pixel of an edge chunk, skipped
+          gx = px;
+          ly = row;
+          const T a = tre[warp][lx], b = tim[warp][lyy];
+          if (MANDEL) {
+            x = T(0);
+            y = T(0);
+            cr = a;
+            ci = b;
+          } else {
+            x = a;
+            y = b;
+          }
+          alive = 1u;
+          cnt = 0;
+        }
+      }
+      next_idx += take;
+    }
+    if (__all_sync(kFull, gx < 0)) break;  // nothing left anywhere for this warp
+
+    // ---- iterate until at least TH lanes have finished (or all remaining lanes, at the end)
+    for (;;) {
 #pragma unroll
-    for (int j = 0; j < K; ++j) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
-    n += K;
-    if (!__any_sync(kFull, alive)) {
-      more = false;
-      break;
+      for (int j = 0; j < K; ++j) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
+      const bool fin = (gx >= 0) && (!alive || cnt >= max_iter);
+      const unsigned fm = __ballot_sync(kFull, fin);
+      const unsigned held = __ballot_sync(kFull, gx >= 0);
+      const int nf = __popc(fm);
+      if (nf >= TH || (nf > 0 && (exhausted || nf == __popc(held)))) {
+        if (fin) {
+          const int count = cnt < max_iter ? cnt : max_iter;
+          const int64_t off = (int64_t)ly * g.W + gx;
+          g.counts[off] = (uint16_t)count;
+          if (COLOR) g.rgba[off] = colour_of(spal, pal, count, max_iter);
+          gx = -1;
+          alive = 0u;
+        }
+        break;
+      }
     }
   }
-  if (more) {
-    for (; n < max_iter; ++n) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
+
+  // ---- self-reset of the workspace by the last CTA to finish
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&ws->done_ctas, 1u);
+    if (prev == gridDim.x - 1) {
+      ws->next_chunk = 0u;
+      ws->done_ctas = 0u;
+      __threadfence();
+    }
   }
-  if (!inside) return;
-  const int count = cnt < max_iter ? cnt : max_iter;
-  const int64_t off = (int64_t)(frame0 + f) * g.frame_stride + (int64_t)ly * g.W + px;
-  g.counts[off] = (uint16_t)count;
-  if (COLOR) g.rgba[off] = colour_of(spal, pal, count, max_iter);
 }
 
 // ----------------------------------------------------------------------------------

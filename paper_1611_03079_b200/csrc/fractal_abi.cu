@@ -4,8 +4,12 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
+#include <utility>
 
 #include "../../include/fractal.h"
 #include "escape_kernels.cuh"
@@ -92,14 +96,17 @@ fr::Geom make_geom(fr_window win, int32_t width, int32_t height, int32_t max_ite
   return g;
 }
 
+constexpr int kStaticK = 4;     // iterations per vote block, static kernel
+constexpr int kFramesPerCta = 16;  // frames of a path chunk rendered per CTA (static kernel)
+
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int NC>
 cudaError_t launch_tiles_t(const fr::Geom& g, const fr::Palette& pal, const fr::CList<NC>& cs,
                            int n_frames, int frame0, cudaStream_t s) {
-  constexpr int K = 8;
   const int64_t tiles = (int64_t)g.tiles_x * ((g.rows + fr::kTileH - 1) / fr::kTileH);
-  dim3 grid((unsigned)tiles, (unsigned)n_frames, 1);
-  fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, K, NC>
-      <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0);
+  const int fpc = n_frames < kFramesPerCta ? n_frames : kFramesPerCta;
+  dim3 grid((unsigned)tiles, (unsigned)((n_frames + fpc - 1) / fpc), 1);
+  fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, kStaticK, NC>
+      <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -128,6 +135,121 @@ cudaError_t launch_tiles(fr_mode mode, bool color, const fr::Geom& g, const fr::
   return launch_tiles_mode<MANDEL, false, NC>(mode, g, pal, cs, n_frames, frame0, s);
 }
 
+// ---------------------------------------------------------------- refill kernel (R)
+// Per-(device, stream) workspace holding the chunk counter.  Created (zeroed) on first
+// use outside any graph capture; the kernel's last CTA resets it, so later launches on
+// the same stream -- including CUDA-graph replays -- find it zeroed.
+std::mutex g_ws_mutex;
+std::map<std::pair<int, uintptr_t>, fr::Workspace*> g_ws;
+
+cudaError_t workspace_for(cudaStream_t s, fr::Workspace** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(g_ws_mutex);
+  auto key = std::make_pair(dev, (uintptr_t)s);
+  auto it = g_ws.find(key);
+  if (it != g_ws.end()) {
+    *out = it->second;
+    return cudaSuccess;
+  }
+  fr::Workspace* w = nullptr;
+  e = cudaMalloc(&w, sizeof(fr::Workspace));
+  if (e != cudaSuccess) return e;
+  e = cudaMemset(w, 0, sizeof(fr::Workspace));
+  if (e != cudaSuccess) return e;
+  g_ws[key] = w;
+  *out = w;
+  return cudaSuccess;
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH>
+cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c, cudaStream_t s) {
+  fr::Workspace* ws = nullptr;
+  cudaError_t e = workspace_for(s, &ws);
+  if (e != cudaSuccess) return e;
+  auto kern = fr::escape_refill_kernel<T, STRICT, MANDEL, COLOR, K, TH>;
+  static int occ = 0;  // per instantiation
+  if (occ == 0) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, fr::kThreads, 0);
+    if (e != cudaSuccess || occ <= 0) occ = 1;
+  }
+  const unsigned n_chunks =
+      (unsigned)((int64_t)g.tiles_x * ((g.rows + fr::kTileH - 1) / fr::kTileH));
+  int64_t blocks = (int64_t)sm_count() * occ;
+  const int64_t need = (n_chunks + fr::kThreads / 32 - 1) / (fr::kThreads / 32);
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  kern<<<(unsigned)blocks, fr::kThreads, 0, s>>>(g, pal, c, ws, n_chunks);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+// Tuning variants of the refill kernel for FP32_FAST (FRACTAL_REFILL=K,TH); default 8,8.
+int refill_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("FRACTAL_REFILL");
+    v = 0;
+    if (e) {
+      if (!std::strcmp(e, "4,4")) v = 1;
+      else if (!std::strcmp(e, "4,8")) v = 2;
+      else if (!std::strcmp(e, "8,16")) v = 3;
+      else if (!std::strcmp(e, "8,1")) v = 4;
+      else if (!std::strcmp(e, "16,8")) v = 5;
+    }
+  }
+  return v;
+}
+
+template <bool MANDEL, bool COLOR>
+cudaError_t launch_refill_mode(fr_mode mode, const fr::Geom& g, const fr::Palette& pal,
+                               double2 c, cudaStream_t s) {
+  switch (mode) {
+    case FR_FP32_FAST:
+      switch (refill_variant()) {
+        case 1: return launch_refill_t<float, false, MANDEL, COLOR, 4, 4>(g, pal, c, s);
+        case 2: return launch_refill_t<float, false, MANDEL, COLOR, 4, 8>(g, pal, c, s);
+        case 3: return launch_refill_t<float, false, MANDEL, COLOR, 8, 16>(g, pal, c, s);
+        case 4: return launch_refill_t<float, false, MANDEL, COLOR, 8, 1>(g, pal, c, s);
+        case 5: return launch_refill_t<float, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
+        default: return launch_refill_t<float, false, MANDEL, COLOR, 8, 8>(g, pal, c, s);
+      }
+    case FR_FP32_STRICT:
+      return launch_refill_t<float, true, MANDEL, COLOR, 8, 8>(g, pal, c, s);
+    case FR_FP64_FAST:
+      return launch_refill_t<double, false, MANDEL, COLOR, 8, 8>(g, pal, c, s);
+    case FR_FP64_STRICT:
+      return launch_refill_t<double, true, MANDEL, COLOR, 8, 8>(g, pal, c, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// Scheduling policy for single frames: FRACTAL_SCHED=static|refill overrides; default
+// refill for max_iter >= 256 (heavy-tailed counts), static otherwise.
+bool use_refill(int max_iter) {
+  static int forced = -2;
+  if (forced == -2) {
+    const char* e = std::getenv("FRACTAL_SCHED");
+    forced = -1;
+    if (e && !std::strcmp(e, "static")) forced = 0;
+    if (e && !std::strcmp(e, "refill")) forced = 1;
+  }
+  if (forced >= 0) return forced == 1;
+  return max_iter >= 256;
+}
+
 bool mode_valid(fr_mode m) {
   return m == FR_FP32_FAST || m == FR_FP32_STRICT || m == FR_FP64_FAST || m == FR_FP64_STRICT;
 }
@@ -148,10 +270,22 @@ fr_status render_frame(bool mandel, fr_complex c, fr_window win, int32_t width, 
   if (st != FR_OK) return st;
   if (rows == 0) return FR_OK;  // this rank holds no band
   const fr::Geom g = make_geom(win, width, height, max_iter, bands, rows, out_counts, out_rgba);
+  cudaError_t e;
+  if (use_refill(max_iter)) {
+    const double2 cc = make_double2(c.re, c.im);
+    const bool col = pal != nullptr;
+    if (mandel)
+      e = col ? launch_refill_mode<true, true>(mode, g, p, cc, stream)
+              : launch_refill_mode<true, false>(mode, g, p, cc, stream);
+    else
+      e = col ? launch_refill_mode<false, true>(mode, g, p, cc, stream)
+              : launch_refill_mode<false, false>(mode, g, p, cc, stream);
+    return cuda_status(e);
+  }
   fr::CList<1> cs;
   cs.c[0] = make_double2(c.re, c.im);
-  cudaError_t e = mandel ? launch_tiles<true, 1>(mode, pal != nullptr, g, p, cs, 1, 0, stream)
-                         : launch_tiles<false, 1>(mode, pal != nullptr, g, p, cs, 1, 0, stream);
+  e = mandel ? launch_tiles<true, 1>(mode, pal != nullptr, g, p, cs, 1, 0, stream)
+             : launch_tiles<false, 1>(mode, pal != nullptr, g, p, cs, 1, 0, stream);
   return cuda_status(e);
 }
 
