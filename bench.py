@@ -20,7 +20,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -34,7 +33,8 @@ FRAMES_PER_RANK = 512
 W_PX, H_PX, MAX_ITER = 1920, 1080, 100
 RADIUS = 0.7885
 SM_COUNT, FP32_LANES_PER_SM, FP64_LANES_PER_SM = 148, 128, 64
-INSTR_PER_ITER = 6  # issue slots per pixel-iteration at the roofline
+ALG_OPS_PER_ITER = 4  # FMA-pipe ops per pixel-iteration, algorithmic minimum
+SURVEY_OPS_PER_ITER = 6  # SURVEY §8(d)'s per-unit figure (per-iteration test included)
 
 
 def dist_env():
@@ -59,60 +59,57 @@ def path_for(world: int, rank: int):
 
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    """Samples SM clock and throttle reasons DURING the timed region via NVML (every
+    ~10 ms; the B200_PROFILING.md clocks line, without nvidia-smi's 100 ms floor)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.01):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.period = period_s
+        self.samples = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self._nvml = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self._nvml
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, rs))
+            except Exception:
+                pass
+            self._stop.wait(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._nvml is not None:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx.append(float(f[2]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"],
+                    "samples": 0}
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm for sm, _ in self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
+                "source": "NVML, 10 ms"}
 
 
 # --------------------------------------------------------------------------- CPU oracle
@@ -266,15 +263,16 @@ def main():
     # ---- roofline of the dominant (only) kernel: escape_tile_kernel
     peaks = measured_peaks()
     f_max = float(peaks.get("sm_max_mhz", 1965.0))
-    peak_gpix = SM_COUNT * FP32_LANES_PER_SM * f_max * 1e6 / INSTR_PER_ITER / 1e9
+    peak_gpix = SM_COUNT * FP32_LANES_PER_SM * f_max * 1e6 / ALG_OPS_PER_ITER / 1e9
     kavg = statistics.mean(kernel_ms)
     achieved = iters_per_step / (kavg * 1e-3) / 1e9
     roof = {"bound": "alu", "achieved": achieved, "peak": peak_gpix, "unit": "Gpixel-iter/s",
             "frac": achieved / peak_gpix, "traffic": None,
             "kernel": "fr::escape_tile_kernel<float,fast,julia,path>",
             "peak_basis": f"{SM_COUNT} SMs x {FP32_LANES_PER_SM} FP32 lanes x {f_max:.0f} MHz "
-                          f"(MEASURED_PEAKS.json sm_max_mhz) / {INSTR_PER_ITER} issue slots per "
-                          "pixel-iteration",
+                          f"(MEASURED_PEAKS.json sm_max_mhz) / {ALG_OPS_PER_ITER} FMA-pipe ops "
+                          "per pixel-iteration (DESIGN.md §5)",
+            "frac_6op_survey": achieved * ALG_OPS_PER_ITER / SURVEY_OPS_PER_ITER / peak_gpix,
             "kernel_ms_avg": kavg}
     if clocks.get("sm_mhz"):
         roof["frac_at_measured_clock"] = achieved / (peak_gpix * clocks["sm_mhz"] / f_max)
@@ -413,9 +411,11 @@ def extras(fr, W, torch):
         ms = a.elapsed_time(b) / reps
         s = int((out.view(torch.int16).to(torch.int64) & 0xFFFF).sum().item())
         lanes = FP64_LANES_PER_SM if prec == 64 else FP32_LANES_PER_SM
-        peak = SM_COUNT * lanes * f_max * 1e6 / INSTR_PER_ITER / 1e9
+        peak = SM_COUNT * lanes * f_max * 1e6 / ALG_OPS_PER_ITER / 1e9
         res[name] = {"ms": ms, "gpix_iter_s": s / (ms * 1e-3) / 1e9, "pixel_iters": s,
-                     "frac_of_alu_peak": s / (ms * 1e-3) / 1e9 / peak, "mode": mode.name,
+                     "frac_of_alu_peak": s / (ms * 1e-3) / 1e9 / peak,
+                     "frac_6op_survey": s / (ms * 1e-3) / 1e9 / peak * ALG_OPS_PER_ITER
+                     / SURVEY_OPS_PER_ITER, "mode": mode.name,
                      "fused_colorize": bool(pal), "reps": reps,
                      "note": "back-to-back launches, CUDA events"}
         del out, rgba

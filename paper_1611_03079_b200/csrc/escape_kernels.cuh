@@ -39,9 +39,13 @@ struct Geom {
   uchar4* rgba;   // nullptr unless colour levels are fused
 };
 
-template <int NC>
+// Julia C values of a path chunk, already in the kernel's state representation
+// (rounded once to T on the host; doubled in FAST modes -- exact), so the kernel does no
+// per-frame conversion.
+template <class T, int NC>
 struct CList {
-  double2 c[NC];
+  T re[NC];
+  T im[NC];
 };
 
 // ----------------------------------------------------------------------------------
@@ -111,6 +115,18 @@ struct Iter;
 template <>
 struct Iter<float, true> {
   static constexpr float kLim = 4.0f;
+  __device__ __forceinline__ static float mag(float x, float y) {
+    return __fadd_rn(__fmul_rn(x, x), __fmul_rn(y, y));
+  }
+  __device__ __forceinline__ static void core(float& x, float& y, float cr, float ci) {
+    const float xx = __fmul_rn(x, x);
+    const float yy = __fmul_rn(y, y);
+    const float xy = __fmul_rn(x, y);
+    const float t = __fsub_rn(xx, yy);
+    const float s = __fadd_rn(xy, xy);
+    x = __fadd_rn(t, cr);
+    y = __fadd_rn(s, ci);
+  }
   __device__ __forceinline__ static void step(float& x, float& y, float cr, float ci,
                                               unsigned& alive, int& cnt) {
     const float xx = __fmul_rn(x, x);
@@ -128,6 +144,16 @@ struct Iter<float, true> {
 template <>
 struct Iter<float, false> {
   static constexpr float kLim = 16.0f;
+  __device__ __forceinline__ static float mag(float X, float Y) {
+    return __fmaf_rn(X, X, __fmul_rn(Y, Y));
+  }
+  __device__ __forceinline__ static void core(float& X, float& Y, float CR2, float CI2) {
+    const float YY = __fmul_rn(Y, Y);
+    const float Tm = __fmaf_rn(X, X, -YY);
+    const float Yn = __fmaf_rn(X, Y, CI2);
+    X = __fmaf_rn(Tm, 0.5f, CR2);
+    Y = Yn;
+  }
   __device__ __forceinline__ static void step(float& X, float& Y, float CR2, float CI2,
                                               unsigned& alive, int& cnt) {
     const float YY = __fmul_rn(Y, Y);
@@ -143,6 +169,18 @@ struct Iter<float, false> {
 template <>
 struct Iter<double, true> {
   static constexpr double kLim = 4.0;
+  __device__ __forceinline__ static double mag(double x, double y) {
+    return __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+  }
+  __device__ __forceinline__ static void core(double& x, double& y, double cr, double ci) {
+    const double xx = __dmul_rn(x, x);
+    const double yy = __dmul_rn(y, y);
+    const double xy = __dmul_rn(x, y);
+    const double t = __dsub_rn(xx, yy);
+    const double s = __dadd_rn(xy, xy);
+    x = __dadd_rn(t, cr);
+    y = __dadd_rn(s, ci);
+  }
   __device__ __forceinline__ static void step(double& x, double& y, double cr, double ci,
                                               unsigned& alive, int& cnt) {
     const double xx = __dmul_rn(x, x);
@@ -160,6 +198,16 @@ struct Iter<double, true> {
 template <>
 struct Iter<double, false> {
   static constexpr double kLim = 16.0;
+  __device__ __forceinline__ static double mag(double X, double Y) {
+    return __fma_rn(X, X, __dmul_rn(Y, Y));
+  }
+  __device__ __forceinline__ static void core(double& X, double& Y, double CR2, double CI2) {
+    const double YY = __dmul_rn(Y, Y);
+    const double Tm = __fma_rn(X, X, -YY);
+    const double Yn = __fma_rn(X, Y, CI2);
+    X = __fma_rn(Tm, 0.5, CR2);
+    Y = Yn;
+  }
   __device__ __forceinline__ static void step(double& X, double& Y, double CR2, double CI2,
                                               unsigned& alive, int& cnt) {
     const double YY = __dmul_rn(Y, Y);
@@ -202,7 +250,7 @@ __device__ __forceinline__ uchar4 colour_of(const uchar4* spal, const Palette& p
 // ----------------------------------------------------------------------------------
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int NC>
 __global__ void __launch_bounds__(kThreads)
-escape_tile_kernel(const Geom g, const Palette pal, const CList<NC> cs, int frame0,
+escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int frame0,
                    int n_frames, int fpc) {
   __shared__ uchar4 spal[COLOR ? 256 : 1];
   __shared__ T sre[kTileW];
@@ -246,9 +294,8 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<NC> cs, int fram
     } else {
       x = are;
       y = aim;
-      const double2 c = cs.c[NC == 1 ? 0 : f];
-      cr = to_state<T, STRICT>(c.x);
-      ci = to_state<T, STRICT>(c.y);
+      cr = cs.re[NC == 1 ? 0 : f];
+      ci = cs.im[NC == 1 ? 0 : f];
     }
     unsigned alive = inside ? 1u : 0u;
     int cnt = 0;
@@ -276,23 +323,31 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<NC> cs, int fram
 }
 
 // ----------------------------------------------------------------------------------
-// Persistent lane-refill kernel (R) for one frame with a heavy-tailed count
-// distribution (SURVEY §7 hard part 1).  Each warp owns a 32x8-pixel chunk at a time,
-// taken from a global atomic chunk counter (self-resetting workspace).  Every lane
-// iterates its own pixel in blocks of K (exact per-iteration count); when at least TH
-// lanes have finished, the finished lanes store their count (and colour) and take the
-// next pixels of the chunk (prefix rank over the finished lanes), grabbing a new chunk
-// when it is exhausted.  SIMT lanes therefore stay busy whatever the neighbours' counts.
+// Persistent lane-refill kernel (R) for one frame whose counts are heavy-tailed or long
+// (SURVEY §7 hard part 1).  Each warp owns a 32x8-pixel chunk at a time, taken from a
+// global atomic chunk counter (self-resetting workspace).  Every lane iterates its own
+// pixel in unrolled blocks of K; at a block end the lanes whose pixel finished store
+// the count (and colour) and, once at least TH lanes are free, take the next pixels of
+// the chunk by prefix rank, grabbing a new chunk when it is exhausted.  SIMT lanes
+// therefore stay busy whatever their neighbours' counts.
+//
+// AMORT = false: exact escape test every iteration (sticky predicate + increment).
+// AMORT = true : the block runs the bare Z^2+C core (4 FP ops fast, 7 strict) and tests
+//   |Z|^2 once at the block end; a lane that escaped inside the block replays the block
+//   from its saved start state with the per-iteration test to recover the exact index.
+//   Exact given escape monotonicity: with |C| <= 1.99 (checked on the host) an orbit
+//   with |Z_n|^2 > 4 satisfies |Z_{n+1}| >= |Z_n|^2 - |C| - err > 2 forever after
+//   (DESIGN.md "Escape-monotonicity lemma"), so the block-end test cannot miss an escape.
 // ----------------------------------------------------------------------------------
 struct Workspace {
   unsigned int next_chunk;
-  unsigned int done_ctas;
+  unsigned int done_warps;
   unsigned int pad[30];
 };
 
-template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH>
+template <class T, bool STRICT, bool MANDEL, bool COLOR, bool AMORT, int K, int TH>
 __global__ void __launch_bounds__(kThreads)
-escape_refill_kernel(const Geom g, const Palette pal, const double2 c, Workspace* ws,
+escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Workspace* ws,
                      unsigned n_chunks) {
   __shared__ uchar4 spal[COLOR ? 256 : 1];
   __shared__ T tre[kThreads / 32][kTileW];
@@ -301,33 +356,30 @@ escape_refill_kernel(const Geom g, const Palette pal, const double2 c, Workspace
     spal[threadIdx.x] = pal.e[threadIdx.x];
     __syncthreads();
   }
+  using It = Iter<T, STRICT>;
+  constexpr int kChunk = kTileW * kTileH;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int max_iter = g.max_iter;
-  T jcr = T(0), jci = T(0);
-  if (!MANDEL) {
-    jcr = to_state<T, STRICT>(c.x);
-    jci = to_state<T, STRICT>(c.y);
-  }
 
-  // warp-uniform chunk state
-  int chunk_x0 = 0, chunk_y0 = 0;  // pixel origin of the current chunk
-  int next_idx = kTileW * kTileH;  // next undispensed pixel of the chunk (256 = exhausted)
-  bool exhausted = false;          // no more chunks
+  // warp-uniform state
+  int chunk_x0 = 0, chunk_y0 = 0;
+  int next_idx = kChunk;   // next undispensed pixel of the chunk (kChunk = exhausted)
+  bool exhausted = false;  // the global chunk counter ran past the frame
+  unsigned need = kFull;   // lanes that need a pixel
 
   // per-lane pixel state
   T x = T(0), y = T(0), cr = jcr, ci = jci;
+  T x0 = T(0), y0 = T(0);  // AMORT: state at the start of the current block
   unsigned alive = 0u;
-  int cnt = 0;
-  int gx = -1, ly = -1;  // gx < 0: lane holds no pixel
+  int cnt = 0;             // exact: leading iterations with |Z|^2 <= 4; AMORT: iterations done
+  int64_t off = -1;        // output offset of the lane's pixel; < 0: no pixel
 
   for (;;) {
-    // ---- assignment: free lanes take the next pixels of the chunk (prefix rank)
-    for (;;) {
-      const unsigned free_mask = __ballot_sync(kFull, gx < 0);
-      if (free_mask == 0u || exhausted) break;
-      if (next_idx >= kTileW * kTileH) {
+    // ---- hand the next pixels of the chunk to the lanes in `need` (prefix rank)
+    while (need != 0u && !exhausted) {
+      if (next_idx >= kChunk) {
         unsigned cid = 0;
         if (lane == 0) cid = atomicAdd(&ws->next_chunk, 1u);
         cid = __shfl_sync(kFull, cid, 0);
@@ -336,8 +388,7 @@ escape_refill_kernel(const Geom g, const Palette pal, const double2 c, Workspace
           break;
         }
         const int cty = (int)(cid / (unsigned)g.tiles_x);
-        const int ctx = (int)cid - cty * g.tiles_x;
-        chunk_x0 = ctx * kTileW;
+        chunk_x0 = ((int)cid - cty * g.tiles_x) * kTileW;
         chunk_y0 = cty * kTileH;
         __syncwarp();
         tre[warp][lane] = to_state<T, STRICT>(pixel_re(g, min(chunk_x0 + lane, g.W - 1)));
@@ -347,19 +398,19 @@ escape_refill_kernel(const Geom g, const Palette pal, const double2 c, Workspace
         __syncwarp();
         next_idx = 0;
       }
-      const int avail = kTileW * kTileH - next_idx;
-      const int nfree = __popc(free_mask);
-      const int take = nfree < avail ? nfree : avail;
-      const int rank = __popc(free_mask & lt_mask);
-      if (((free_mask >> lane) & 1u) && rank < take) {
+      const int avail = kChunk - next_idx;
+      const int rank = __popc(need & lt_mask);
+      const bool mine = (need >> lane) & 1u;
+      bool got = false;
+      if (mine && rank < avail) {
         const int idx = next_idx + rank;
         const int lx = idx & (kTileW - 1);
         const int lyy = idx >> 5;
         const int px = chunk_x0 + lx;
         const int row = chunk_y0 + lyy;
         if (px < g.W && row < g.rows) {  // else: off-frame pixel of an edge chunk, skipped
-          gx = px;
-          ly = row;
+          got = true;
+          off = (int64_t)row * g.W + px;
           const T a = tre[warp][lx], b = tim[warp][lyy];
           if (MANDEL) {
             x = T(0);
@@ -374,40 +425,78 @@ escape_refill_kernel(const Geom g, const Palette pal, const double2 c, Workspace
           cnt = 0;
         }
       }
-      next_idx += take;
+      const int nneed = __popc(need);
+      next_idx += nneed < avail ? nneed : avail;
+      need = __ballot_sync(kFull, mine && !got);
     }
-    if (__all_sync(kFull, gx < 0)) break;  // nothing left anywhere for this warp
+    const int n_held = __popc(__ballot_sync(kFull, off >= 0));
+    if (n_held == 0) break;  // chunks exhausted and every pixel stored
+    const bool held = off >= 0;
 
-    // ---- iterate until at least TH lanes have finished (or all remaining lanes, at the end)
-    for (;;) {
+    // ---- iterate in blocks of K until >= TH lanes finished (or all held lanes, or the end)
+    bool fin;
+    unsigned fm;
+    if (!AMORT) {
+      for (;;) {
 #pragma unroll
-      for (int j = 0; j < K; ++j) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
-      const bool fin = (gx >= 0) && (!alive || cnt >= max_iter);
-      const unsigned fm = __ballot_sync(kFull, fin);
-      const unsigned held = __ballot_sync(kFull, gx >= 0);
-      const int nf = __popc(fm);
-      if (nf >= TH || (nf > 0 && (exhausted || nf == __popc(held)))) {
-        if (fin) {
-          const int count = cnt < max_iter ? cnt : max_iter;
-          const int64_t off = (int64_t)ly * g.W + gx;
-          g.counts[off] = (uint16_t)count;
-          if (COLOR) g.rgba[off] = colour_of(spal, pal, count, max_iter);
-          gx = -1;
-          alive = 0u;
+        for (int j = 0; j < K; ++j) It::step(x, y, cr, ci, alive, cnt);
+        fin = held && (!alive || cnt >= max_iter);
+        fm = __ballot_sync(kFull, fin);
+        const int nf = __popc(fm);
+        if (nf >= TH || (nf != 0 && (exhausted || nf == n_held))) break;
+      }
+    } else {
+      // a finished lane freezes (x0, y0, cnt) until the warp services it
+      bool done = false, esc = false;
+      for (;;) {
+        if (!done) {
+          x0 = x;
+          y0 = y;
         }
-        break;
+#pragma unroll
+        for (int j = 0; j < K; ++j) It::core(x, y, cr, ci);
+        const bool e = !(It::mag(x, y) <= It::kLim);  // unordered: NaN/inf count as escaped
+        if (held && !done && (e || cnt + K >= max_iter)) {
+          done = true;
+          esc = e;
+        }
+        if (!done) cnt += K;
+        fm = __ballot_sync(kFull, held && done);
+        if (fm != 0u) {
+          const int nf = __popc(fm);
+          if (nf >= TH || exhausted || nf == n_held) break;
+        }
+      }
+      fin = held && done;
+      if (fin) {
+        // exact index: replay the block from its start state with the per-iteration test
+        T rx = x0, ry = y0;
+        unsigned ra = 1u;
+        int rc = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) It::step(rx, ry, cr, ci, ra, rc);
+        // rc < K: escaped at cnt + rc; rc == K: escaped at the block-end state (cnt + K)
+        // if `esc`, else the iteration limit was reached without escape.
+        cnt = esc ? cnt + rc : max_iter;
       }
     }
+    if (fin) {
+      const int count = cnt < max_iter ? cnt : max_iter;
+      g.counts[off] = (uint16_t)count;
+      if (COLOR) g.rgba[off] = colour_of(spal, pal, count, max_iter);
+      off = -1;
+      alive = 0u;
+    }
+    need = fm;
   }
 
-  // ---- self-reset of the workspace by the last CTA to finish
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  // ---- self-reset of the workspace by the last warp to finish
+  if (lane == 0) {
     __threadfence();
-    const unsigned prev = atomicAdd(&ws->done_ctas, 1u);
-    if (prev == gridDim.x - 1) {
+    const unsigned prev = atomicAdd(&ws->done_warps, 1u);
+    if (prev == gridDim.x * (kThreads / 32) - 1) {
       ws->next_chunk = 0u;
-      ws->done_ctas = 0u;
+      ws->done_warps = 0u;
       __threadfence();
     }
   }

@@ -100,39 +100,61 @@ constexpr int kStaticK = 4;     // iterations per vote block, static kernel
 constexpr int kFramesPerCta = 16;  // frames of a path chunk rendered per CTA (static kernel)
 
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int NC>
-cudaError_t launch_tiles_t(const fr::Geom& g, const fr::Palette& pal, const fr::CList<NC>& cs,
+cudaError_t launch_tiles_t(const fr::Geom& g, const fr::Palette& pal, const fr::CList<T, NC>& cs,
                            int n_frames, int frame0, cudaStream_t s) {
   const int64_t tiles = (int64_t)g.tiles_x * ((g.rows + fr::kTileH - 1) / fr::kTileH);
   const int fpc = n_frames < kFramesPerCta ? n_frames : kFramesPerCta;
   dim3 grid((unsigned)tiles, (unsigned)((n_frames + fpc - 1) / fpc), 1);
-  fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, kStaticK, NC>
+  fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, (sizeof(T) == 8 ? 2 * kStaticK : kStaticK), NC>
       <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
+// C in the kernel's state representation (C_T = RN_T(C), on the host;
+// FAST modes keep 2C, an exact doubling).
+template <class T, bool STRICT>
+T state_of(double v) {
+  const T t = (T)v;  // round to nearest (default FP environment)
+  return STRICT ? t : t + t;
+}
+
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int NC>
+cudaError_t launch_tiles_conv(const fr::Geom& g, const fr::Palette& pal, const fr_complex* c,
+                              int n_frames, int frame0, cudaStream_t s) {
+  fr::CList<T, NC>* cs = new (std::nothrow) fr::CList<T, NC>;
+  if (!cs) return cudaErrorMemoryAllocation;
+  for (int k = 0; k < n_frames && !MANDEL; ++k) {
+    cs->re[k] = state_of<T, STRICT>(c[k].re);
+    cs->im[k] = state_of<T, STRICT>(c[k].im);
+  }
+  if (MANDEL) cs->re[0] = cs->im[0] = T(0);
+  const cudaError_t e = launch_tiles_t<T, STRICT, MANDEL, COLOR, NC>(g, pal, *cs, n_frames, frame0, s);
+  delete cs;
+  return e;
+}
+
 template <bool MANDEL, bool COLOR, int NC>
 cudaError_t launch_tiles_mode(fr_mode mode, const fr::Geom& g, const fr::Palette& pal,
-                              const fr::CList<NC>& cs, int n_frames, int frame0,
-                              cudaStream_t s) {
+                              const fr_complex* c, int n_frames, int frame0, cudaStream_t s) {
   switch (mode) {
     case FR_FP32_FAST:
-      return launch_tiles_t<float, false, MANDEL, COLOR, NC>(g, pal, cs, n_frames, frame0, s);
+      return launch_tiles_conv<float, false, MANDEL, COLOR, NC>(g, pal, c, n_frames, frame0, s);
     case FR_FP32_STRICT:
-      return launch_tiles_t<float, true, MANDEL, COLOR, NC>(g, pal, cs, n_frames, frame0, s);
+      return launch_tiles_conv<float, true, MANDEL, COLOR, NC>(g, pal, c, n_frames, frame0, s);
     case FR_FP64_FAST:
-      return launch_tiles_t<double, false, MANDEL, COLOR, NC>(g, pal, cs, n_frames, frame0, s);
+      return launch_tiles_conv<double, false, MANDEL, COLOR, NC>(g, pal, c, n_frames, frame0, s);
     case FR_FP64_STRICT:
-      return launch_tiles_t<double, true, MANDEL, COLOR, NC>(g, pal, cs, n_frames, frame0, s);
+      return launch_tiles_conv<double, true, MANDEL, COLOR, NC>(g, pal, c, n_frames, frame0, s);
   }
   return cudaErrorInvalidValue;
 }
 
 template <bool MANDEL, int NC>
 cudaError_t launch_tiles(fr_mode mode, bool color, const fr::Geom& g, const fr::Palette& pal,
-                         const fr::CList<NC>& cs, int n_frames, int frame0, cudaStream_t s) {
-  if (color) return launch_tiles_mode<MANDEL, true, NC>(mode, g, pal, cs, n_frames, frame0, s);
-  return launch_tiles_mode<MANDEL, false, NC>(mode, g, pal, cs, n_frames, frame0, s);
+                         const fr_complex* c, int n_frames, int frame0, cudaStream_t s) {
+  if (color) return launch_tiles_mode<MANDEL, true, NC>(mode, g, pal, c, n_frames, frame0, s);
+  return launch_tiles_mode<MANDEL, false, NC>(mode, g, pal, c, n_frames, frame0, s);
 }
 
 // ---------------------------------------------------------------- refill kernel (R)
@@ -174,12 +196,14 @@ int sm_count() {
   return sms;
 }
 
-template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH>
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH, bool AMORT = false>
 cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c, cudaStream_t s) {
+  const T jcr = MANDEL ? T(0) : state_of<T, STRICT>(c.x);
+  const T jci = MANDEL ? T(0) : state_of<T, STRICT>(c.y);
   fr::Workspace* ws = nullptr;
   cudaError_t e = workspace_for(s, &ws);
   if (e != cudaSuccess) return e;
-  auto kern = fr::escape_refill_kernel<T, STRICT, MANDEL, COLOR, K, TH>;
+  auto kern = fr::escape_refill_kernel<T, STRICT, MANDEL, COLOR, AMORT, K, TH>;
   static int occ = 0;  // per instantiation
   if (occ == 0) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, fr::kThreads, 0);
@@ -191,23 +215,25 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
   const int64_t need = (n_chunks + fr::kThreads / 32 - 1) / (fr::kThreads / 32);
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, fr::kThreads, 0, s>>>(g, pal, c, ws, n_chunks);
+  kern<<<(unsigned)blocks, fr::kThreads, 0, s>>>(g, pal, jcr, jci, ws, n_chunks);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
-// Tuning variants of the refill kernel for FP32_FAST (FRACTAL_REFILL=K,TH); default 8,8.
+// Tuning variants of the refill kernel for FP32_FAST (FRACTAL_REFILL=K,TH); default 16,16.
 int refill_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("FRACTAL_REFILL");
     v = 0;
     if (e) {
-      if (!std::strcmp(e, "4,4")) v = 1;
-      else if (!std::strcmp(e, "4,8")) v = 2;
-      else if (!std::strcmp(e, "8,16")) v = 3;
-      else if (!std::strcmp(e, "8,1")) v = 4;
-      else if (!std::strcmp(e, "16,8")) v = 5;
+      if (!std::strcmp(e, "8,8")) v = 1;
+      else if (!std::strcmp(e, "16,8")) v = 2;
+      else if (!std::strcmp(e, "16,24")) v = 3;
+      else if (!std::strcmp(e, "32,16")) v = 4;
+      else if (!std::strcmp(e, "8,16")) v = 5;
+      else if (!std::strcmp(e, "16,1")) v = 6;
+      else if (!std::strcmp(e, "16,4")) v = 7;
     }
   }
   return v;
@@ -219,35 +245,74 @@ cudaError_t launch_refill_mode(fr_mode mode, const fr::Geom& g, const fr::Palett
   switch (mode) {
     case FR_FP32_FAST:
       switch (refill_variant()) {
-        case 1: return launch_refill_t<float, false, MANDEL, COLOR, 4, 4>(g, pal, c, s);
-        case 2: return launch_refill_t<float, false, MANDEL, COLOR, 4, 8>(g, pal, c, s);
-        case 3: return launch_refill_t<float, false, MANDEL, COLOR, 8, 16>(g, pal, c, s);
-        case 4: return launch_refill_t<float, false, MANDEL, COLOR, 8, 1>(g, pal, c, s);
-        case 5: return launch_refill_t<float, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
-        default: return launch_refill_t<float, false, MANDEL, COLOR, 8, 8>(g, pal, c, s);
+        case 1: return launch_refill_t<float, false, MANDEL, COLOR, 8, 8>(g, pal, c, s);
+        case 2: return launch_refill_t<float, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
+        case 3: return launch_refill_t<float, false, MANDEL, COLOR, 16, 24>(g, pal, c, s);
+        case 4: return launch_refill_t<float, false, MANDEL, COLOR, 32, 16>(g, pal, c, s);
+        case 5: return launch_refill_t<float, false, MANDEL, COLOR, 8, 16>(g, pal, c, s);
+        case 6: return launch_refill_t<float, false, MANDEL, COLOR, 16, 1>(g, pal, c, s);
+        case 7: return launch_refill_t<float, false, MANDEL, COLOR, 16, 4>(g, pal, c, s);
+        default: return launch_refill_t<float, false, MANDEL, COLOR, 16, 16>(g, pal, c, s);
       }
     case FR_FP32_STRICT:
-      return launch_refill_t<float, true, MANDEL, COLOR, 8, 8>(g, pal, c, s);
+      return launch_refill_t<float, true, MANDEL, COLOR, 16, 16>(g, pal, c, s);
     case FR_FP64_FAST:
-      return launch_refill_t<double, false, MANDEL, COLOR, 8, 8>(g, pal, c, s);
+      return launch_refill_t<double, false, MANDEL, COLOR, 16, 16>(g, pal, c, s);
     case FR_FP64_STRICT:
-      return launch_refill_t<double, true, MANDEL, COLOR, 8, 8>(g, pal, c, s);
+      return launch_refill_t<double, true, MANDEL, COLOR, 16, 16>(g, pal, c, s);
   }
   return cudaErrorInvalidValue;
 }
 
+template <bool MANDEL, bool COLOR>
+cudaError_t launch_amort_mode(fr_mode mode, const fr::Geom& g, const fr::Palette& pal,
+                              double2 c, cudaStream_t s) {
+  switch (mode) {
+    case FR_FP32_FAST:
+      return launch_refill_t<float, false, MANDEL, COLOR, 16, 1, true>(g, pal, c, s);
+    case FR_FP32_STRICT:
+      return launch_refill_t<float, true, MANDEL, COLOR, 16, 1, true>(g, pal, c, s);
+    case FR_FP64_FAST:
+      return launch_refill_t<double, false, MANDEL, COLOR, 16, 1, true>(g, pal, c, s);
+    case FR_FP64_STRICT:
+      return launch_refill_t<double, true, MANDEL, COLOR, 16, 1, true>(g, pal, c, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// Escape-monotonicity precondition of the amortised kernel: every C of
+// the frame satisfies |C| <= 1.989 (Julia: the constant; Mandelbrot: the window's
+// corners bound every pixel centre).
+bool monotone_ok(bool mandel, fr_complex c, fr_window w) {
+  const double lim = 1.989;
+  if (!mandel) return std::hypot(c.re, c.im) <= lim;
+  for (int sx = -1; sx <= 1; sx += 2)
+    for (int sy = -1; sy <= 1; sy += 2)
+      if (std::hypot(w.center_re + sx * w.half_w, w.center_im + sy * w.half_h) > lim)
+        return false;
+  return true;
+}
+
 // Scheduling policy for single frames: FRACTAL_SCHED=static|refill overrides; default
 // refill for max_iter >= 256 (heavy-tailed counts), static otherwise.
-bool use_refill(int max_iter) {
+enum Sched { kStatic = 0, kRefill = 1, kAmort = 2 };
+
+Sched choose_sched(bool mandel, fr_complex c, fr_window w, int max_iter) {
   static int forced = -2;
   if (forced == -2) {
     const char* e = std::getenv("FRACTAL_SCHED");
     forced = -1;
-    if (e && !std::strcmp(e, "static")) forced = 0;
-    if (e && !std::strcmp(e, "refill")) forced = 1;
+    if (e && !std::strcmp(e, "static")) forced = kStatic;
+    if (e && !std::strcmp(e, "refill")) forced = kRefill;
+    if (e && !std::strcmp(e, "amort")) forced = kAmort;
   }
-  if (forced >= 0) return forced == 1;
-  return max_iter >= 256;
+  const bool mono = monotone_ok(mandel, c, w);
+  if (forced >= 0) return (forced == kAmort && !mono) ? kRefill : (Sched)forced;
+  if (max_iter < 256) return kStatic;
+  // Long, low-divergence counts (deep Mandelbrot zooms) amortise the escape test;
+  // heavy-tailed Julia frames keep the exact per-iteration test with lane refill.
+  if (mandel && mono && max_iter >= 1000) return kAmort;
+  return kRefill;
 }
 
 bool mode_valid(fr_mode m) {
@@ -271,21 +336,28 @@ fr_status render_frame(bool mandel, fr_complex c, fr_window win, int32_t width, 
   if (rows == 0) return FR_OK;  // this rank holds no band
   const fr::Geom g = make_geom(win, width, height, max_iter, bands, rows, out_counts, out_rgba);
   cudaError_t e;
-  if (use_refill(max_iter)) {
+  const Sched sched = choose_sched(mandel, c, win, max_iter);
+  if (sched != kStatic) {
     const double2 cc = make_double2(c.re, c.im);
     const bool col = pal != nullptr;
-    if (mandel)
+    if (sched == kAmort) {
+      if (mandel)
+        e = col ? launch_amort_mode<true, true>(mode, g, p, cc, stream)
+                : launch_amort_mode<true, false>(mode, g, p, cc, stream);
+      else
+        e = col ? launch_amort_mode<false, true>(mode, g, p, cc, stream)
+                : launch_amort_mode<false, false>(mode, g, p, cc, stream);
+    } else if (mandel) {
       e = col ? launch_refill_mode<true, true>(mode, g, p, cc, stream)
               : launch_refill_mode<true, false>(mode, g, p, cc, stream);
-    else
+    } else {
       e = col ? launch_refill_mode<false, true>(mode, g, p, cc, stream)
               : launch_refill_mode<false, false>(mode, g, p, cc, stream);
+    }
     return cuda_status(e);
   }
-  fr::CList<1> cs;
-  cs.c[0] = make_double2(c.re, c.im);
-  e = mandel ? launch_tiles<true, 1>(mode, pal != nullptr, g, p, cs, 1, 0, stream)
-             : launch_tiles<false, 1>(mode, pal != nullptr, g, p, cs, 1, 0, stream);
+  e = mandel ? launch_tiles<true, 1>(mode, pal != nullptr, g, p, &c, 1, 0, stream)
+             : launch_tiles<false, 1>(mode, pal != nullptr, g, p, &c, 1, 0, stream);
   return cuda_status(e);
 }
 
@@ -331,15 +403,12 @@ fr_status julia_render_path(const fr_complex* c_host, int32_t n_frames, fr_windo
   if (st != FR_OK) return st;
   const fr::Geom g = make_geom(win, width, height, max_iter, fr_bands{0, 1, 0}, height,
                                out_counts, out_rgba);
-  fr::CList<fr::kMaxPathChunk>* cs = new (std::nothrow) fr::CList<fr::kMaxPathChunk>;
-  if (!cs) return FR_ERR_CUDA;
   cudaError_t e = cudaSuccess;
   for (int32_t f0 = 0; f0 < n_frames && e == cudaSuccess; f0 += fr::kMaxPathChunk) {
     const int nf = n_frames - f0 < fr::kMaxPathChunk ? n_frames - f0 : fr::kMaxPathChunk;
-    for (int k = 0; k < nf; ++k) cs->c[k] = make_double2(c_host[f0 + k].re, c_host[f0 + k].im);
-    e = launch_tiles<false, fr::kMaxPathChunk>(mode, pal != nullptr, g, p, *cs, nf, f0, stream);
+    e = launch_tiles<false, fr::kMaxPathChunk>(mode, pal != nullptr, g, p, c_host + f0, nf, f0,
+                                               stream);
   }
-  delete cs;
   return cuda_status(e);
 }
 

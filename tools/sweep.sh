@@ -3,14 +3,13 @@
 TAG=${1:-sweep}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2>&1
-for S in auto static refill; do
+for S in auto static refill amort; do
   FRACTAL_SCHED=$S timeout 900 python -m pytest tests -m gpu -q -x -k "not largest and not cfg5 and not cfg4_strict" > gpurun_out/pytest_${TAG}_$S.log 2>&1
   echo "rc=$?" >> gpurun_out/pytest_${TAG}_$S.log
 done
-for S in static refill; do
+for S in static refill amort; do
   FRACTAL_SCHED=$S timeout 300 python tools/perf_probe.py cfg2 cfg3 cfg5 > gpurun_out/perf_${TAG}_$S.log 2>&1
 done
-for V in 4,4 4,8 8,16 8,1 16,8; do
+for V in 16,1 16,4 16,8 8,8; do
   FRACTAL_SCHED=refill FRACTAL_REFILL=$V timeout 300 python tools/perf_probe.py cfg3 > gpurun_out/perf_${TAG}_refill_$V.log 2>&1
 done
-timeout 300 python tools/perf_probe.py cfg4 > gpurun_out/perf_${TAG}_cfg4.log 2>&1
