@@ -272,7 +272,7 @@ def main():
             "peak_basis": f"{SM_COUNT} SMs x {FP32_LANES_PER_SM} FP32 lanes x {f_max:.0f} MHz "
                           f"(MEASURED_PEAKS.json sm_max_mhz) / {ALG_OPS_PER_ITER} FMA-pipe ops "
                           "per pixel-iteration (DESIGN.md §5)",
-            "frac_6op_survey": achieved * ALG_OPS_PER_ITER / SURVEY_OPS_PER_ITER / peak_gpix,
+            "frac_6op_survey": achieved * SURVEY_OPS_PER_ITER / ALG_OPS_PER_ITER / peak_gpix,
             "kernel_ms_avg": kavg}
     if clocks.get("sm_mhz"):
         roof["frac_at_measured_clock"] = achieved / (peak_gpix * clocks["sm_mhz"] / f_max)
@@ -414,8 +414,8 @@ def extras(fr, W, torch):
         peak = SM_COUNT * lanes * f_max * 1e6 / ALG_OPS_PER_ITER / 1e9
         res[name] = {"ms": ms, "gpix_iter_s": s / (ms * 1e-3) / 1e9, "pixel_iters": s,
                      "frac_of_alu_peak": s / (ms * 1e-3) / 1e9 / peak,
-                     "frac_6op_survey": s / (ms * 1e-3) / 1e9 / peak * ALG_OPS_PER_ITER
-                     / SURVEY_OPS_PER_ITER, "mode": mode.name,
+                     "frac_6op_survey": s / (ms * 1e-3) / 1e9 / peak * SURVEY_OPS_PER_ITER
+                     / ALG_OPS_PER_ITER, "mode": mode.name,
                      "fused_colorize": bool(pal), "reps": reps,
                      "note": "back-to-back launches, CUDA events"}
         del out, rgba
