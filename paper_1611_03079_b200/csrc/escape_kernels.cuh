@@ -4,6 +4,7 @@
 // §Readings.  Nothing here is shared with oracle/ (which is plain C, test-only).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace fr {
@@ -240,6 +241,125 @@ __device__ __forceinline__ uchar4 colour_of(const uchar4* spal, const Palette& p
 }
 
 // ----------------------------------------------------------------------------------
+// Whole vote loop of the FAST fp32 iteration in one PTX block: the sticky alive
+// predicate stays a predicate across blocks (no predicate<->register round trip), and
+// the loop test is one vote + one compare.  Runs blocks of K iterations while any lane
+// of the warp is alive and fewer than `kfull` (a multiple of K) iterations have run.
+// Returns the number of iterations run (warp-uniform); cnt / alive updated per lane.
+// ----------------------------------------------------------------------------------
+#define FR_FAST_STEP                                 \
+  "mul.rn.f32 yy, %1, %1;\n\t"                       \
+  "fma.rn.f32 m, %0, %0, yy;\n\t"                    \
+  "setp.le.and.f32 pa, m, 0f41800000, pa;\n\t"       \
+  "@pa add.s32 %2, %2, 1;\n\t"                       \
+  "neg.f32 yy, yy;\n\t"                              \
+  "fma.rn.f32 t, %0, %0, yy;\n\t"                    \
+  "fma.rn.f32 %1, %0, %1, %7;\n\t"                   \
+  "fma.rn.f32 %0, t, 0f3F000000, %6;\n\t"
+
+template <int K>
+__device__ __forceinline__ int fast_vote_loop_f32(float& x, float& y, int& cnt, unsigned& alive,
+                                                  float cr2, float ci2, int kfull);
+
+template <>
+__device__ __forceinline__ int fast_vote_loop_f32<2>(float& x, float& y, int& cnt,
+                                                     unsigned& alive, float cr2, float ci2,
+                                                     int kfull) {
+  int n;
+  asm volatile(
+      "{\n\t.reg .pred pa, pm;\n\t.reg .f32 yy, m, t;\n\t"
+      "setp.ne.u32 pa, %3, 0;\n\tmov.u32 %4, 0;\n\t"
+      "setp.gt.s32 pm, %5, 0;\n\t@!pm bra FR_K2_DONE;\n"
+      "FR_K2_LOOP:\n\t" FR_FAST_STEP FR_FAST_STEP
+      "add.s32 %4, %4, 2;\n\t"
+      "vote.sync.any.pred pm, pa, 0xffffffff;\n\t"
+      "setp.lt.and.s32 pm, %4, %5, pm;\n\t"
+      "@pm bra FR_K2_LOOP;\n"
+      "FR_K2_DONE:\n\t"
+      "selp.u32 %3, 1, 0, pa;\n\t}"
+      : "+f"(x), "+f"(y), "+r"(cnt), "+r"(alive), "=r"(n)
+      : "r"(kfull), "f"(cr2), "f"(ci2));
+  return n;
+}
+
+template <>
+__device__ __forceinline__ int fast_vote_loop_f32<4>(float& x, float& y, int& cnt,
+                                                     unsigned& alive, float cr2, float ci2,
+                                                     int kfull) {
+  int n;
+  asm volatile(
+      "{\n\t.reg .pred pa, pm;\n\t.reg .f32 yy, m, t;\n\t"
+      "setp.ne.u32 pa, %3, 0;\n\tmov.u32 %4, 0;\n\t"
+      "setp.gt.s32 pm, %5, 0;\n\t@!pm bra FR_K4_DONE;\n"
+      "FR_K4_LOOP:\n\t" FR_FAST_STEP FR_FAST_STEP FR_FAST_STEP FR_FAST_STEP
+      "add.s32 %4, %4, 4;\n\t"
+      "vote.sync.any.pred pm, pa, 0xffffffff;\n\t"
+      "setp.lt.and.s32 pm, %4, %5, pm;\n\t"
+      "@pm bra FR_K4_LOOP;\n"
+      "FR_K4_DONE:\n\t"
+      "selp.u32 %3, 1, 0, pa;\n\t}"
+      : "+f"(x), "+f"(y), "+r"(cnt), "+r"(alive), "=r"(n)
+      : "r"(kfull), "f"(cr2), "f"(ci2));
+  return n;
+}
+#undef FR_FAST_STEP
+
+// Two independent orbits per lane (same pixel, two frames of a path): instruction-level
+// parallelism for the FP pipe and one vote per block for both.
+#define FR_FAST_STEP2                                \
+  "mul.rn.f32 yy, %1, %1;\n\t"                       \
+  "mul.rn.f32 yy2, %6, %6;\n\t"                      \
+  "fma.rn.f32 m, %0, %0, yy;\n\t"                    \
+  "fma.rn.f32 m2, %5, %5, yy2;\n\t"                  \
+  "setp.le.and.f32 pa, m, 0f41800000, pa;\n\t"       \
+  "setp.le.and.f32 pb, m2, 0f41800000, pb;\n\t"      \
+  "@pa add.s32 %2, %2, 1;\n\t"                       \
+  "@pb add.s32 %7, %7, 1;\n\t"                       \
+  "neg.f32 yy, yy;\n\t"                              \
+  "neg.f32 yy2, yy2;\n\t"                            \
+  "fma.rn.f32 t, %0, %0, yy;\n\t"                    \
+  "fma.rn.f32 t2, %5, %5, yy2;\n\t"                  \
+  "fma.rn.f32 %1, %0, %1, %13;\n\t"                  \
+  "fma.rn.f32 %6, %5, %6, %15;\n\t"                  \
+  "fma.rn.f32 %0, t, 0f3F000000, %12;\n\t"           \
+  "fma.rn.f32 %5, t2, 0f3F000000, %14;\n\t"
+
+template <int K>
+__device__ __forceinline__ int fast_vote_loop2_f32(float& x, float& y, int& cnt, unsigned& alive,
+                                                   float& x2, float& y2, int& cnt2,
+                                                   unsigned& alive2, float cr2, float ci2,
+                                                   float cr2b, float ci2b, int kfull);
+
+template <>
+__device__ __forceinline__ int fast_vote_loop2_f32<4>(float& x, float& y, int& cnt,
+                                                      unsigned& alive, float& x2, float& y2,
+                                                      int& cnt2, unsigned& alive2, float cr2,
+                                                      float ci2, float cr2b, float ci2b,
+                                                      int kfull) {
+  int n;
+  asm volatile(
+      "{\n\t.reg .pred pa, pb, pm;\n\t.reg .f32 yy, m, t, yy2, m2, t2;\n\t"
+      "setp.ne.u32 pa, %3, 0;\n\tsetp.ne.u32 pb, %8, 0;\n\tmov.u32 %4, 0;\n\t"
+      "setp.gt.s32 pm, %9, 0;\n\t@!pm bra FR_K4B_DONE;\n"
+      "FR_K4B_LOOP:\n\t" FR_FAST_STEP2 FR_FAST_STEP2 FR_FAST_STEP2 FR_FAST_STEP2
+      "add.s32 %4, %4, 4;\n\t"
+      "or.pred pm, pa, pb;\n\t"
+      "vote.sync.any.pred pm, pm, 0xffffffff;\n\t"
+      "setp.lt.and.s32 pm, %4, %9, pm;\n\t"
+      "@pm bra FR_K4B_LOOP;\n"
+      "FR_K4B_DONE:\n\t"
+      "selp.u32 %3, 1, 0, pa;\n\tselp.u32 %8, 1, 0, pb;\n\t}"
+      : "+f"(x), "+f"(y), "+r"(cnt), "+r"(alive), "=r"(n), "+f"(x2), "+f"(y2), "+r"(cnt2),
+        "+r"(alive2)
+      : "r"(kfull), "r"(0), "r"(0), "f"(cr2), "f"(ci2), "f"(cr2b), "f"(ci2b));
+  return n;
+}
+#undef FR_FAST_STEP2
+
+template <class T, bool STRICT, int K>
+constexpr bool kAsmLoop = std::is_same<T, float>::value && !STRICT && (K == 2 || K == 4);
+
+// ----------------------------------------------------------------------------------
 // Static-tile kernel (S): one pixel per thread, 8x4 warp tiles in a 32x8 CTA tile.  The
 // CTA computes its tile's axis values once (32 re + 8 im, binary64 -> state type) into
 // shared memory and then renders a GROUP of frames of the path chunk for that tile
@@ -280,11 +400,42 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
   const T are = sre[cx];
   const T aim = sim[cy];
   const int max_iter = g.max_iter;
+  const int kfull = max_iter - max_iter % K;  // iterations run in whole K-blocks
   const int f0 = blockIdx.y * fpc;
   const int f1 = min(f0 + fpc, n_frames);
-  const int64_t pix_off = (int64_t)ly * g.W + px;
+  const int64_t stride = g.frame_stride;
+  uint16_t* outp = g.counts + (int64_t)(frame0 + f0) * stride + (int64_t)ly * g.W + px;
+  uchar4* outc = COLOR ? g.rgba + (outp - g.counts) : nullptr;
 
-  for (int f = f0; f < f1; ++f) {
+  int f = f0;
+  if constexpr (kAsmLoop<T, STRICT, K> && K == 4 && !MANDEL && NC > 1) {
+    // two frames per lane (ILP); the remaining odd frame goes through the loop below
+    for (; f + 1 < f1; f += 2) {
+      float x = are, y = aim, x2 = are, y2 = aim;
+      unsigned alive = inside ? 1u : 0u, alive2 = alive;
+      int cnt = 0, cnt2 = 0;
+      int n = fast_vote_loop2_f32<4>(x, y, cnt, alive, x2, y2, cnt2, alive2, cs.re[f], cs.im[f],
+                                     cs.re[f + 1], cs.im[f + 1], kfull);
+      if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
+        for (; n < max_iter; ++n) {
+          Iter<T, STRICT>::step(x, y, cs.re[f], cs.im[f], alive, cnt);
+          Iter<T, STRICT>::step(x2, y2, cs.re[f + 1], cs.im[f + 1], alive2, cnt2);
+        }
+      }
+      if (inside) {
+        const int c1 = min(cnt, max_iter), c2 = min(cnt2, max_iter);
+        outp[0] = (uint16_t)c1;
+        outp[stride] = (uint16_t)c2;
+        if (COLOR) {
+          outc[0] = colour_of(spal, pal, c1, max_iter);
+          outc[stride] = colour_of(spal, pal, c2, max_iter);
+        }
+      }
+      outp += 2 * stride;
+      if (COLOR) outc += 2 * stride;
+    }
+  }
+  for (; f < f1; ++f) {
     T x, y, cr, ci;
     if (MANDEL) {
       x = T(0);
@@ -299,26 +450,28 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
     }
     unsigned alive = inside ? 1u : 0u;
     int cnt = 0;
-    int n = 0;
-    bool more = true;
-    while (n + K <= max_iter) {
+    int n;
+    if constexpr (kAsmLoop<T, STRICT, K>) {
+      n = fast_vote_loop_f32<K>(x, y, cnt, alive, cr, ci, kfull);
+    } else {
+      n = 0;
+      while (n < kfull) {
 #pragma unroll
-      for (int j = 0; j < K; ++j) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
-      n += K;
-      if (!__any_sync(kFull, alive)) {
-        more = false;
-        break;
+        for (int j = 0; j < K; ++j) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
+        n += K;
+        if (!__any_sync(kFull, alive)) break;
       }
     }
-    if (more) {
+    if (kfull != max_iter && n == kfull && __any_sync(kFull, alive)) {
       for (; n < max_iter; ++n) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
     }
     if (inside) {
-      const int count = cnt < max_iter ? cnt : max_iter;
-      const int64_t off = (int64_t)(frame0 + f) * g.frame_stride + pix_off;
-      g.counts[off] = (uint16_t)count;
-      if (COLOR) g.rgba[off] = colour_of(spal, pal, count, max_iter);
+      const int count = min(cnt, max_iter);
+      *outp = (uint16_t)count;
+      if (COLOR) *outc = colour_of(spal, pal, count, max_iter);
     }
+    outp += stride;
+    if (COLOR) outc += stride;
   }
 }
 
@@ -348,14 +501,19 @@ struct Workspace {
 template <class T, bool STRICT, bool MANDEL, bool COLOR, bool AMORT, int K, int TH>
 __global__ void __launch_bounds__(kThreads)
 escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Workspace* ws,
-                     unsigned n_chunks) {
+                     unsigned n_chunks, unsigned chunks_per_cta) {
   __shared__ uchar4 spal[COLOR ? 256 : 1];
   __shared__ T tre[kThreads / 32][kTileW];
   __shared__ T tim[kThreads / 32][kTileH];
-  if (COLOR) {
-    spal[threadIdx.x] = pal.e[threadIdx.x];
-    __syncthreads();
-  }
+  __shared__ unsigned s_next;  // CTA-local chunk source (chunks_per_cta > 0)
+  if (COLOR) spal[threadIdx.x] = pal.e[threadIdx.x];
+  if (threadIdx.x == 0) s_next = 0u;
+  __syncthreads();
+  // chunk source: CTA-local range [c_lo, c_hi) when chunks_per_cta > 0 (the hardware
+  // block scheduler balances CTAs and a CTA's drain overlaps its SM neighbours'
+  // work), else the global counter of the persistent grid
+  const unsigned c_lo = chunks_per_cta ? blockIdx.x * chunks_per_cta : 0u;
+  const unsigned c_hi = chunks_per_cta ? min(n_chunks, c_lo + chunks_per_cta) : n_chunks;
   using It = Iter<T, STRICT>;
   constexpr int kChunk = kTileW * kTileH;
   const int lane = threadIdx.x & 31;
@@ -381,9 +539,10 @@ escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
     while (need != 0u && !exhausted) {
       if (next_idx >= kChunk) {
         unsigned cid = 0;
-        if (lane == 0) cid = atomicAdd(&ws->next_chunk, 1u);
+        if (lane == 0) cid = chunks_per_cta ? c_lo + atomicAdd(&s_next, 1u)
+                                            : atomicAdd(&ws->next_chunk, 1u);
         cid = __shfl_sync(kFull, cid, 0);
-        if (cid >= n_chunks) {
+        if (cid >= c_hi) {
           exhausted = true;
           break;
         }
@@ -490,8 +649,8 @@ escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
     need = fm;
   }
 
-  // ---- self-reset of the workspace by the last warp to finish
-  if (lane == 0) {
+  // ---- self-reset of the workspace by the last warp to finish (persistent grid)
+  if (!chunks_per_cta && lane == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(&ws->done_warps, 1u);
     if (prev == gridDim.x * (kThreads / 32) - 1) {

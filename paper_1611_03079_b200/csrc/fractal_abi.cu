@@ -96,7 +96,16 @@ fr::Geom make_geom(fr_window win, int32_t width, int32_t height, int32_t max_ite
   return g;
 }
 
-constexpr int kStaticK = 4;     // iterations per vote block, static kernel
+// iterations per vote block of the static kernel (FRACTAL_STATIC_K=2|4 for fp32 fast)
+constexpr int kStaticK = 4;
+int static_k() {
+  static int k = 0;
+  if (k == 0) {
+    const char* e = std::getenv("FRACTAL_STATIC_K");
+    k = (e && !std::strcmp(e, "2")) ? 2 : 4;
+  }
+  return k;
+}
 constexpr int kFramesPerCta = 16;  // frames of a path chunk rendered per CTA (static kernel)
 
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int NC>
@@ -105,8 +114,12 @@ cudaError_t launch_tiles_t(const fr::Geom& g, const fr::Palette& pal, const fr::
   const int64_t tiles = (int64_t)g.tiles_x * ((g.rows + fr::kTileH - 1) / fr::kTileH);
   const int fpc = n_frames < kFramesPerCta ? n_frames : kFramesPerCta;
   dim3 grid((unsigned)tiles, (unsigned)((n_frames + fpc - 1) / fpc), 1);
-  fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, (sizeof(T) == 8 ? 2 * kStaticK : kStaticK), NC>
-      <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);
+  if (sizeof(T) == 4 && !STRICT && static_k() == 2)
+    fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, 2, NC>
+        <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);
+  else
+    fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, (sizeof(T) == 8 ? 2 * kStaticK : kStaticK), NC>
+        <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -196,26 +209,45 @@ int sm_count() {
   return sms;
 }
 
+// Chunks per CTA of the CTA-local refill grid (FRACTAL_REFILL_CPC; 0 = persistent grid
+// with a global chunk counter).
+int refill_cpc() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("FRACTAL_REFILL_CPC");
+    v = e ? std::atoi(e) : 16;
+    if (v < 0) v = 16;
+  }
+  return v;
+}
+
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH, bool AMORT = false>
 cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c, cudaStream_t s) {
   const T jcr = MANDEL ? T(0) : state_of<T, STRICT>(c.x);
   const T jci = MANDEL ? T(0) : state_of<T, STRICT>(c.y);
-  fr::Workspace* ws = nullptr;
-  cudaError_t e = workspace_for(s, &ws);
-  if (e != cudaSuccess) return e;
   auto kern = fr::escape_refill_kernel<T, STRICT, MANDEL, COLOR, AMORT, K, TH>;
-  static int occ = 0;  // per instantiation
-  if (occ == 0) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, fr::kThreads, 0);
-    if (e != cudaSuccess || occ <= 0) occ = 1;
-  }
   const unsigned n_chunks =
       (unsigned)((int64_t)g.tiles_x * ((g.rows + fr::kTileH - 1) / fr::kTileH));
-  int64_t blocks = (int64_t)sm_count() * occ;
-  const int64_t need = (n_chunks + fr::kThreads / 32 - 1) / (fr::kThreads / 32);
-  if (blocks > need) blocks = need;
-  if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, fr::kThreads, 0, s>>>(g, pal, jcr, jci, ws, n_chunks);
+  const int cpc = refill_cpc();
+  cudaError_t e;
+  if (cpc > 0) {
+    const unsigned blocks = (n_chunks + cpc - 1) / cpc;
+    kern<<<blocks, fr::kThreads, 0, s>>>(g, pal, jcr, jci, nullptr, n_chunks, (unsigned)cpc);
+  } else {
+    fr::Workspace* ws = nullptr;
+    e = workspace_for(s, &ws);
+    if (e != cudaSuccess) return e;
+    static int occ = 0;  // per instantiation
+    if (occ == 0) {
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, fr::kThreads, 0);
+      if (e != cudaSuccess || occ <= 0) occ = 1;
+    }
+    int64_t blocks = (int64_t)sm_count() * occ;
+    const int64_t need = (n_chunks + fr::kThreads / 32 - 1) / (fr::kThreads / 32);
+    if (blocks > need) blocks = need;
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, fr::kThreads, 0, s>>>(g, pal, jcr, jci, ws, n_chunks, 0u);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
