@@ -128,6 +128,18 @@ fr_status mandelbrot_param_map(fr_window win, int32_t width, int32_t height, int
 fr_status colorize(const uint16_t* counts, int64_t n_pixels, int32_t max_iter,
                    const fr_palette* pal, uint8_t* out_rgba, fr_stream stream);
 
+/* The paper's prescribed C-path: "the parameter moves clockwise along the cardioid
+ * f(t) = ([2 cos t - cos 2t]/a, [2 sin t - sin 2t]/a), where a has the value 3.9"; a = 4
+ * is the main-cardioid border; "if we let the size of the cardioid increase gradually
+ * (by decreasing the values of a above), almost all relevant parameter values ... will be
+ * traversed after a few trips".  Step rule (clockwise = decreasing t):
+ * C_k = f(t_k, a_k); t_{k+1} = t_k - dt; when t_{k+1} <= -2 pi it wraps (+2 pi) and
+ * a_{k+1} = max(a_k - da_per_rev, a_floor).  Host-only (no GPU work): fills out_host[n]
+ * (HOST memory) for julia_render_path.  Errors: n < 0, non-finite inputs, a0 <= 0,
+ * a_floor <= 0, dt < 0, da_per_rev < 0 -> FR_ERR_INVALID_ARG. */
+fr_status fr_cardioid_path(double t0, double a0, double dt, double da_per_rev, double a_floor,
+                           int32_t n, fr_complex* out_host);
+
 /* Rows a rank holds under `bands` for a frame of `height` rows; -1 if invalid. */
 int64_t fr_band_local_rows(int32_t height, fr_bands bands);
 

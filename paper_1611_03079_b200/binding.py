@@ -70,7 +70,7 @@ STATUS = {0: "FR_OK", 1: "FR_ERR_INVALID_ARG", 2: "FR_ERR_TOO_LARGE", 3: "FR_ERR
 
 # Functions declared in include/fractal.h (checked by tests/test_abi.py).
 EXPORTS = ("julia_render", "julia_render_ex", "julia_render_path", "mandelbrot_param_map",
-           "colorize", "fr_band_local_rows", "fr_band_global_row", "fr_status_str",
+           "colorize", "fr_cardioid_path", "fr_band_local_rows", "fr_band_global_row", "fr_status_str",
            "fr_last_cuda_error", "fr_launch_count", "fr_version")
 
 
@@ -97,6 +97,9 @@ def load():
         for f in ("julia_render", "julia_render_ex", "julia_render_path", "mandelbrot_param_map",
                   "colorize"):
             getattr(lib, f).restype = st
+        f64 = ctypes.c_double
+        lib.fr_cardioid_path.argtypes = [f64, f64, f64, f64, f64, i32, vp]
+        lib.fr_cardioid_path.restype = st
         lib.fr_band_local_rows.argtypes = [i32, _Bands]
         lib.fr_band_local_rows.restype = i64
         lib.fr_band_global_row.argtypes = [i32, _Bands, i64]
@@ -161,6 +164,18 @@ class _PalHolder:
         inter = np.asarray(interior, dtype=np.uint8).reshape(4)
         self.buf = ent
         self.c = _Palette(ent.ctypes.data, ent.shape[0], (ctypes.c_uint8 * 4)(*inter.tolist()))
+
+
+def cardioid_path(n: int, t0: float = 0.0, a0: float = 3.9, dt: float = 2 * np.pi / 600,
+                  da_per_rev: float = 0.05, a_floor: float = 3.5) -> np.ndarray:
+    """The paper's cardioid C-path with the shrinking-a sweep: complex128 [n]
+    (host; feed it to julia_render_path).  Defaults: SPEC S:321 (600 frames per
+    revolution, a from 3.9 down by 0.05 per revolution to 3.5)."""
+    out = np.empty(max(n, 0), dtype=np.complex128)
+    rc = load().fr_cardioid_path(float(t0), float(a0), float(dt), float(da_per_rev),
+                                 float(a_floor), int(n), ctypes.c_void_p(out.ctypes.data))
+    _check(rc, "fr_cardioid_path")
+    return out
 
 
 def band_local_rows(height: int, bands: Bands = FULL_FRAME) -> int:

@@ -596,13 +596,17 @@ escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
     bool fin;
     unsigned fm;
     if (!AMORT) {
+      // service the warp once `thr` lanes finished: TH normally, 1 once the chunks are
+      // exhausted, and never more than the lanes it holds
+      const int thr = exhausted ? 1 : (TH < n_held ? TH : n_held);
+      const int lim = held ? max_iter : 0x7fffffff;  // lanes without a pixel never finish
+      if (!held) alive = 0u;
       for (;;) {
 #pragma unroll
         for (int j = 0; j < K; ++j) It::step(x, y, cr, ci, alive, cnt);
-        fin = held && (!alive || cnt >= max_iter);
+        fin = held && (!alive || cnt >= lim);
         fm = __ballot_sync(kFull, fin);
-        const int nf = __popc(fm);
-        if (nf >= TH || (nf != 0 && (exhausted || nf == n_held))) break;
+        if (__popc(fm) >= thr) break;
       }
     } else {
       // a finished lane freezes (x0, y0, cnt) until the warp services it

@@ -209,16 +209,18 @@ int sm_count() {
   return sms;
 }
 
-// Chunks per CTA of the CTA-local refill grid (FRACTAL_REFILL_CPC; 0 = persistent grid
-// with a global chunk counter).
-int refill_cpc() {
-  static int v = -1;
-  if (v < 0) {
+// Chunks per CTA of the CTA-local refill grid; 0 = persistent grid with a global chunk
+// counter.  Measured (B200): persistent is faster for heavy-tailed Julia frames (cfg3:
+// 0.30 vs 0.36 ms), CTA-local for long uniform counts (cfg5: 641 vs 663 ms).
+// FRACTAL_REFILL_CPC overrides.
+int refill_cpc(bool amort) {
+  static int v = -2;
+  if (v == -2) {
     const char* e = std::getenv("FRACTAL_REFILL_CPC");
-    v = e ? std::atoi(e) : 16;
-    if (v < 0) v = 16;
+    v = e ? std::atoi(e) : -1;
   }
-  return v;
+  if (v >= 0) return v;
+  return amort ? 16 : 0;
 }
 
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH, bool AMORT = false>
@@ -228,7 +230,7 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
   auto kern = fr::escape_refill_kernel<T, STRICT, MANDEL, COLOR, AMORT, K, TH>;
   const unsigned n_chunks =
       (unsigned)((int64_t)g.tiles_x * ((g.rows + fr::kTileH - 1) / fr::kTileH));
-  const int cpc = refill_cpc();
+  const int cpc = refill_cpc(AMORT);
   cudaError_t e;
   if (cpc > 0) {
     const unsigned blocks = (n_chunks + cpc - 1) / cpc;
@@ -252,7 +254,7 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
   return cudaGetLastError();
 }
 
-// Tuning variants of the refill kernel for FP32_FAST (FRACTAL_REFILL=K,TH); default 16,16.
+// Tuning variants of the refill kernel for FP32_FAST (FRACTAL_REFILL=K,TH); default 16,8.
 int refill_variant() {
   static int v = -1;
   if (v < 0) {
@@ -260,7 +262,7 @@ int refill_variant() {
     v = 0;
     if (e) {
       if (!std::strcmp(e, "8,8")) v = 1;
-      else if (!std::strcmp(e, "16,8")) v = 2;
+      else if (!std::strcmp(e, "16,16")) v = 2;
       else if (!std::strcmp(e, "16,24")) v = 3;
       else if (!std::strcmp(e, "32,16")) v = 4;
       else if (!std::strcmp(e, "8,16")) v = 5;
@@ -278,20 +280,20 @@ cudaError_t launch_refill_mode(fr_mode mode, const fr::Geom& g, const fr::Palett
     case FR_FP32_FAST:
       switch (refill_variant()) {
         case 1: return launch_refill_t<float, false, MANDEL, COLOR, 8, 8>(g, pal, c, s);
-        case 2: return launch_refill_t<float, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
+        case 2: return launch_refill_t<float, false, MANDEL, COLOR, 16, 16>(g, pal, c, s);
         case 3: return launch_refill_t<float, false, MANDEL, COLOR, 16, 24>(g, pal, c, s);
         case 4: return launch_refill_t<float, false, MANDEL, COLOR, 32, 16>(g, pal, c, s);
         case 5: return launch_refill_t<float, false, MANDEL, COLOR, 8, 16>(g, pal, c, s);
         case 6: return launch_refill_t<float, false, MANDEL, COLOR, 16, 1>(g, pal, c, s);
         case 7: return launch_refill_t<float, false, MANDEL, COLOR, 16, 4>(g, pal, c, s);
-        default: return launch_refill_t<float, false, MANDEL, COLOR, 16, 16>(g, pal, c, s);
+        default: return launch_refill_t<float, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
       }
     case FR_FP32_STRICT:
-      return launch_refill_t<float, true, MANDEL, COLOR, 16, 16>(g, pal, c, s);
+      return launch_refill_t<float, true, MANDEL, COLOR, 16, 8>(g, pal, c, s);
     case FR_FP64_FAST:
-      return launch_refill_t<double, false, MANDEL, COLOR, 16, 16>(g, pal, c, s);
+      return launch_refill_t<double, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
     case FR_FP64_STRICT:
-      return launch_refill_t<double, true, MANDEL, COLOR, 16, 16>(g, pal, c, s);
+      return launch_refill_t<double, true, MANDEL, COLOR, 16, 8>(g, pal, c, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -472,6 +474,30 @@ fr_status colorize(const uint16_t* counts, int64_t n_pixels, int32_t max_iter,
         counts, n_pixels, max_iter, p, o);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
+}
+
+fr_status fr_cardioid_path(double t0, double a0, double dt, double da_per_rev, double a_floor,
+                           int32_t n, fr_complex* out_host) {
+  if (n < 0) return FR_ERR_INVALID_ARG;
+  if (!(is_fin(t0) && is_fin(a0) && is_fin(dt) && is_fin(da_per_rev) && is_fin(a_floor)))
+    return FR_ERR_INVALID_ARG;
+  if (!(a0 > 0.0) || !(a_floor > 0.0) || dt < 0.0 || da_per_rev < 0.0) return FR_ERR_INVALID_ARG;
+  if (n == 0) return FR_OK;
+  if (!out_host) return FR_ERR_INVALID_ARG;
+  const double two_pi = 6.283185307179586476925286766559;
+  double t = t0, a = a0;
+  for (int32_t k = 0; k < n; ++k) {
+    const double re = (2.0 * std::cos(t) - std::cos(2.0 * t)) / a;
+    const double im = (2.0 * std::sin(t) - std::sin(2.0 * t)) / a;
+    out_host[k].re = re;
+    out_host[k].im = im;
+    t = t - dt;
+    if (t <= -two_pi) {
+      t += two_pi;
+      a = a - da_per_rev > a_floor ? a - da_per_rev : a_floor;
+    }
+  }
+  return FR_OK;
 }
 
 int64_t fr_band_local_rows(int32_t height, fr_bands bands) {

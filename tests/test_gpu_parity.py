@@ -393,3 +393,18 @@ def test_side_stream_and_launch_count(fr):
     b = gpu_julia(fr, cfg.c, cfg.window, 64, 64, 100, fr.Mode.FP32_STRICT)
     np.testing.assert_array_equal(np16(a), b)
     assert fr.launch_count() == before + 2
+
+
+# ------------------------------------------------------------------ NEXT-2: cardioid path
+def test_cardioid_path_frames_strict(fr):
+    """The paper's own dynamic workload: Julia frames along the a = 3.9 cardioid
+    with the shrinking-a sweep, strict fp32, equal to the oracle frame by frame."""
+    cs = fr.cardioid_path(1300)[::20]  # 65 frames over two revolutions
+    w, h = 320, 180
+    win = W.julia_window(w, h)
+    out = fr.julia_render_path(cs, win, w, h, 100, fr.Mode.FP32_STRICT)
+    torch.cuda.synchronize()
+    got = np16(out)
+    for k in range(len(cs)):
+        ref = oracle.julia(complex(cs[k]), win.center, win.half_w, win.half_h, w, h, 100, 32)
+        np.testing.assert_array_equal(got[k], ref)
