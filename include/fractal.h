@@ -122,6 +122,23 @@ fr_status mandelbrot_param_map(fr_window win, int32_t width, int32_t height, int
                                fr_mode mode, fr_bands bands, uint16_t* out_counts,
                                const fr_palette* pal, uint8_t* out_rgba, fr_stream stream);
 
+/* Other iteration maps (NEXT-3): the paper notes "many other functions yield fruitful
+ * explorations" and shows one in Figure 4, printed garbled as
+ * z^4 + (z^2+1)/(z^2+1) + c; it is read per SPEC S:35 (reading c-14). */
+typedef enum {
+    FR_FN_Z2 = 0,         /* z^2 + c (the main map) */
+    FR_FN_Z4 = 1,         /* z^4 + c */
+    FR_FN_Z4_RATIONAL = 2 /* z^4 + (z^2+1)/(z^2-1) + c; at the pole z^2 = 1, Z -> +inf */
+} fr_function;
+
+/* Julia frame of map `fn` (same count definition, bailout |Z|^2 > 4, map and layout as
+ * julia_render_ex; full frame).  Both modes of a precision run the strict IEEE operation
+ * sequence of reading c-14 (the FAST rescaling applies to z^2 + c only).
+ * Errors as julia_render_ex; unknown fn -> FR_ERR_UNSUPPORTED. */
+fr_status julia_render_fn(fr_function fn, fr_complex c, fr_window win, int32_t width,
+                          int32_t height, int32_t max_iter, fr_mode mode, uint16_t* out_counts,
+                          const fr_palette* pal, uint8_t* out_rgba, fr_stream stream);
+
 /* Standalone colour levels over n_pixels counts.
  *   counts device uint16 [n_pixels], out_rgba device uint8 [n_pixels][4];
  *   n_pixels == 0 is a no-op; counts > max_iter are mapped by the same rule. */

@@ -77,6 +77,12 @@ def _load():
         lib.oracle_pixels_nudged.argtypes = [i32, f64, f64, f64, f64, f64, f64, i64, i64, i32, i32,
                                              vp, vp, i64, i32, vp, i32]
         lib.oracle_pixels_nudged.restype = i32
+        lib.oracle_escape_fn_f32.argtypes = [i32, f32, f32, f32, f32, i32]
+        lib.oracle_escape_fn_f32.restype = i32
+        lib.oracle_escape_fn_f64.argtypes = [i32, f64, f64, f64, f64, i32]
+        lib.oracle_escape_fn_f64.restype = i32
+        lib.oracle_julia_fn.argtypes = [i32, f64, f64, f64, f64, f64, f64, i64, i64, i32, i32, vp]
+        lib.oracle_julia_fn.restype = i32
         _lib = lib
         return lib
 
@@ -227,4 +233,26 @@ def pixels_nudged(kind: str, c: complex, center: complex, half_w: float, half_h:
                                       threads or default_threads())
     if rc != 0:
         raise ValueError("oracle_pixels_nudged: invalid arguments")
+    return out
+
+
+# --------------------------------------------------------------------------- NEXT-3 maps
+FUNCTIONS = {"z2": 0, "z4": 1, "z4_rational": 2}
+
+
+def escape_time_fn(fn: str, z0: complex, c: complex, max_iter: int = 100, precision=64) -> int:
+    """Escape time under z^2+c ('z2'), z^4+c ('z4') or z^4+(z^2+1)/(z^2-1)+c
+    ('z4_rational'; pole -> +inf), reading c-14."""
+    lib = _load()
+    f = lib.oracle_escape_fn_f32 if _prec(precision) == 32 else lib.oracle_escape_fn_f64
+    return int(f(FUNCTIONS[fn], z0.real, z0.imag, c.real, c.imag, int(max_iter)))
+
+
+def julia_fn(fn: str, c: complex, center: complex, half_w: float, half_h: float, width: int,
+             height: int, max_iter: int = 100, precision=32) -> np.ndarray:
+    out = np.empty((height, width), dtype=np.uint16)
+    rc = _load().oracle_julia_fn(FUNCTIONS[fn], c.real, c.imag, center.real, center.imag, half_w,
+                                 half_h, width, height, max_iter, _prec(precision), _ptr(out))
+    if rc != 0:
+        raise ValueError("oracle_julia_fn: invalid arguments")
     return out

@@ -346,3 +346,79 @@ int oracle_distance_pixels(int mandel, double c_re, double c_im, double center_r
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-3: other iteration maps ("many other functions yield fruitful    */
+/* explorations"; Figure 4, garbled as z^4 + (z^2+1)/(z^2+1) + c and   */
+/* read per SPEC S:35 as z^4 + (z^2+1)/(z^2-1) + c; reading c-14). */
+/* fn 0: z^2 + c;  fn 1: z^4 + c;  fn 2: z^4 + (z^2+1)/(z^2-1) + c.           */
+/* Same count definition and bailout |Z_n|^2 > 4.  Operation sequence:        */
+/*   w = z^2 = (xx - yy, xy + xy);  z^4 = w^2 = (wx*wx - wy*wy, p + p),       */
+/*   p = wx*wy;  rational: q = (w + 1)/(w - 1) by the textbook formula        */
+/*   ((a c + b d) + i (b c - a d)) / (c^2 + d^2); pole (c^2 + d^2 == 0):      */
+/*   Z_{n+1} = +inf (escapes at the next test).                     */
+/* ------------------------------------------------------------------------- */
+
+#define DEF_FN_ESCAPE(NAME, T, LIM)                                                   \
+    int NAME(int fn, T zre, T zim, T cre, T cim, int max_iter) {                     \
+        T x = zre, y = zim;                                                           \
+        for (int n = 0; n < max_iter; ++n) {                                          \
+            T xx = x * x;                                                             \
+            T yy = y * y;                                                             \
+            T m = xx + yy;                                                            \
+            if (m > LIM) return n;                                                    \
+            T xy = x * y;                                                             \
+            T wx = xx - yy;                                                           \
+            T wy = xy + xy;                                                           \
+            if (fn == 0) {                                                            \
+                x = wx + cre;                                                         \
+                y = wy + cim;                                                         \
+                continue;                                                             \
+            }                                                                         \
+            T u = wx * wx;                                                            \
+            T v = wy * wy;                                                            \
+            T p = wx * wy;                                                            \
+            T fx = u - v;                                                             \
+            T fy = p + p;                                                             \
+            if (fn == 2) {                                                            \
+                T a = wx + (T)1;                                                      \
+                T c = wx - (T)1;                                                      \
+                T b = wy;                                                             \
+                T d = wy;                                                             \
+                T den = c * c + d * d;                                                \
+                if (den == (T)0) {                                                    \
+                    x = (T)INFINITY;                                                  \
+                    y = (T)0;                                                         \
+                    continue;                                                         \
+                }                                                                     \
+                T qx = (a * c + b * d) / den;                                         \
+                T qy = (b * c - a * d) / den;                                         \
+                fx = fx + qx;                                                         \
+                fy = fy + qy;                                                         \
+            }                                                                         \
+            x = fx + cre;                                                             \
+            y = fy + cim;                                                             \
+        }                                                                             \
+        return max_iter;                                                              \
+    }
+
+DEF_FN_ESCAPE(oracle_escape_fn_f32, float, 4.0f)
+DEF_FN_ESCAPE(oracle_escape_fn_f64, double, 4.0)
+
+/* Julia frame of map fn (single-threaded rows are fine for test sizes). */
+int oracle_julia_fn(int fn, double c_re, double c_im, double center_re, double center_im,
+                    double half_w, double half_h, int64_t width, int64_t height, int max_iter,
+                    int precision, uint16_t* out) {
+    if (!args_ok(precision, width, height, max_iter) || !out || fn < 0 || fn > 2) return -1;
+    for (int64_t py = 0; py < height; ++py)
+        for (int64_t px = 0; px < width; ++px) {
+            double re = oracle_pixel_re(center_re, half_w, width, px);
+            double im = oracle_pixel_im(center_im, half_h, height, py);
+            out[py * width + px] =
+                (uint16_t)(precision == 32
+                               ? oracle_escape_fn_f32(fn, (float)re, (float)im, (float)c_re,
+                                                      (float)c_im, max_iter)
+                               : oracle_escape_fn_f64(fn, re, im, c_re, c_im, max_iter));
+        }
+    return 0;
+}

@@ -34,6 +34,13 @@ class Mode(enum.IntEnum):
     FP64_STRICT = 3
 
 
+class Function(enum.IntEnum):
+    """Iteration maps (NEXT-3; Figure 4, reading c-14)."""
+    Z2 = 0
+    Z4 = 1
+    Z4_RATIONAL = 2
+
+
 class _Complex(ctypes.Structure):
     _fields_ = [("re", ctypes.c_double), ("im", ctypes.c_double)]
 
@@ -70,7 +77,7 @@ STATUS = {0: "FR_OK", 1: "FR_ERR_INVALID_ARG", 2: "FR_ERR_TOO_LARGE", 3: "FR_ERR
 
 # Functions declared in include/fractal.h (checked by tests/test_abi.py).
 EXPORTS = ("julia_render", "julia_render_ex", "julia_render_path", "mandelbrot_param_map",
-           "colorize", "fr_cardioid_path", "fr_band_local_rows", "fr_band_global_row", "fr_status_str",
+           "colorize", "julia_render_fn", "fr_cardioid_path", "fr_band_local_rows", "fr_band_global_row", "fr_status_str",
            "fr_last_cuda_error", "fr_launch_count", "fr_version")
 
 
@@ -94,6 +101,9 @@ def load():
         lib.mandelbrot_param_map.argtypes = [_Window, i32, i32, i32, st, _Bands, vp, P(_Palette),
                                              vp, vp]
         lib.colorize.argtypes = [vp, i64, i32, P(_Palette), vp, vp]
+        lib.julia_render_fn.argtypes = [st, _Complex, _Window, i32, i32, i32, st, vp, P(_Palette),
+                                        vp, vp]
+        lib.julia_render_fn.restype = st
         for f in ("julia_render", "julia_render_ex", "julia_render_path", "mandelbrot_param_map",
                   "colorize"):
             getattr(lib, f).restype = st
@@ -284,3 +294,22 @@ def colorize(counts, max_iter: int, palette, out_rgba=None, stream=None):
     rc = load().colorize(p, n, max_iter, ctypes.byref(pal.c), q, _stream(stream))
     _check(rc, "colorize")
     return out_rgba
+
+
+def julia_render_fn(fn, c: complex, win, width: int, height: int, max_iter: int = 100,
+                    mode: Mode = Mode.FP32_STRICT, out=None, palette=None, out_rgba=None,
+                    stream=None):
+    """Julia frame of another iteration map (z^4 + c, z^4 + (z^2+1)/(z^2-1) + c)."""
+    import torch
+    if out is None:
+        out = torch.empty((height, width), dtype=torch.uint16, device="cuda")
+    pal = _PalHolder(palette) if palette is not None else None
+    if pal is not None and out_rgba is None:
+        out_rgba = torch.empty((height, width, 4), dtype=torch.uint8, device="cuda")
+    p = _dev_ptr(out, "uint16", height * width, "out")
+    q = _dev_ptr(out_rgba, "uint8", height * width * 4, "out_rgba") if out_rgba is not None else None
+    rc = load().julia_render_fn(int(fn), _Complex(complex(c).real, complex(c).imag), _window(win),
+                                width, height, max_iter, int(mode), p,
+                                ctypes.byref(pal.c) if pal else None, q, _stream(stream))
+    _check(rc, "julia_render_fn")
+    return (out, out_rgba) if pal is not None else out

@@ -221,6 +221,69 @@ struct Iter<double, false> {
   }
 };
 
+// NEXT-3 iteration maps (Figure 4, reading c-14), strict op sequence in
+// both modes, identical to the oracle's: w = z^2 = (xx - yy, xy + xy); z^4 = w^2;
+// rational term q = (w + 1)/(w - 1) = ((a c + b d) + i (b c - a d))/(c^2 + d^2) with
+// a = wx + 1, c = wx - 1, b = d = wy; pole (c^2 + d^2 == 0) -> Z_{n+1} = +inf.
+template <class T>
+struct Ops;
+template <>
+struct Ops<float> {
+  __device__ __forceinline__ static float mul(float a, float b) { return __fmul_rn(a, b); }
+  __device__ __forceinline__ static float add(float a, float b) { return __fadd_rn(a, b); }
+  __device__ __forceinline__ static float sub(float a, float b) { return __fsub_rn(a, b); }
+  __device__ __forceinline__ static float div(float a, float b) { return __fdiv_rn(a, b); }
+  __device__ __forceinline__ static void alive(unsigned& al, int& cnt, float m) {
+    alive_step_f32(al, cnt, m, 4.0f);
+  }
+  __device__ __forceinline__ static float inf() { return __int_as_float(0x7f800000); }
+};
+template <>
+struct Ops<double> {
+  __device__ __forceinline__ static double mul(double a, double b) { return __dmul_rn(a, b); }
+  __device__ __forceinline__ static double add(double a, double b) { return __dadd_rn(a, b); }
+  __device__ __forceinline__ static double sub(double a, double b) { return __dsub_rn(a, b); }
+  __device__ __forceinline__ static double div(double a, double b) { return __ddiv_rn(a, b); }
+  __device__ __forceinline__ static void alive(unsigned& al, int& cnt, double m) {
+    alive_step_f64(al, cnt, m, 4.0);
+  }
+  __device__ __forceinline__ static double inf() { return __longlong_as_double(0x7ff0000000000000ll); }
+};
+
+template <class T, int FN>
+struct FnIter {
+  __device__ __forceinline__ static void step(T& x, T& y, T cr, T ci, unsigned& alive, int& cnt) {
+    using O = Ops<T>;
+    const T xx = O::mul(x, x);
+    const T yy = O::mul(y, y);
+    O::alive(alive, cnt, O::add(xx, yy));
+    const T xy = O::mul(x, y);
+    const T wx = O::sub(xx, yy);
+    const T wy = O::add(xy, xy);
+    const T u = O::mul(wx, wx);
+    const T v = O::mul(wy, wy);
+    const T pp = O::mul(wx, wy);
+    T fx = O::sub(u, v);
+    T fy = O::add(pp, pp);
+    if (FN == 2) {
+      const T a = O::add(wx, T(1));
+      const T c = O::sub(wx, T(1));
+      const T den = O::add(O::mul(c, c), O::mul(wy, wy));
+      if (den == T(0)) {
+        x = O::inf();
+        y = T(0);
+        return;
+      }
+      const T qx = O::div(O::add(O::mul(a, c), O::mul(wy, wy)), den);
+      const T qy = O::div(O::sub(O::mul(wy, c), O::mul(a, wy)), den);
+      fx = O::add(fx, qx);
+      fy = O::add(fy, qy);
+    }
+    x = O::add(fx, cr);
+    y = O::add(fy, ci);
+  }
+};
+
 // Initial state for a pixel: STRICT keeps (x, y, cr, ci); FAST keeps the doubled
 // values (exact scaling by 2).  For binary32 the binary64 map value and C are rounded
 // once to nearest (reading c-8).
@@ -368,10 +431,11 @@ constexpr bool kAsmLoop = std::is_same<T, float>::value && !STRICT && (K == 2 ||
 // count is exact per iteration (sticky alive predicate + predicated increment).
 // MANDEL takes C from the pixel and Z_0 = 0.
 // ----------------------------------------------------------------------------------
-template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int NC>
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int NC, int FN = 0>
 __global__ void __launch_bounds__(kThreads)
 escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int frame0,
                    int n_frames, int fpc) {
+  static_assert(FN == 0 || (STRICT && !MANDEL), "map variants: strict Julia frames");
   __shared__ uchar4 spal[COLOR ? 256 : 1];
   __shared__ T sre[kTileW];
   __shared__ T sim[kTileH];
@@ -408,7 +472,7 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
   uchar4* outc = COLOR ? g.rgba + (outp - g.counts) : nullptr;
 
   int f = f0;
-  if constexpr (kAsmLoop<T, STRICT, K> && K == 4 && !MANDEL && NC > 1) {
+  if constexpr (FN == 0 && kAsmLoop<T, STRICT, K> && K == 4 && !MANDEL && NC > 1) {
     // two frames per lane (ILP); the remaining odd frame goes through the loop below
     for (; f + 1 < f1; f += 2) {
       float x = are, y = aim, x2 = are, y2 = aim;
@@ -451,19 +515,20 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
     unsigned alive = inside ? 1u : 0u;
     int cnt = 0;
     int n;
-    if constexpr (kAsmLoop<T, STRICT, K>) {
+    using It = typename std::conditional<FN == 0, Iter<T, STRICT>, FnIter<T, FN>>::type;
+    if constexpr (FN == 0 && kAsmLoop<T, STRICT, K>) {
       n = fast_vote_loop_f32<K>(x, y, cnt, alive, cr, ci, kfull);
     } else {
       n = 0;
       while (n < kfull) {
 #pragma unroll
-        for (int j = 0; j < K; ++j) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
+        for (int j = 0; j < K; ++j) It::step(x, y, cr, ci, alive, cnt);
         n += K;
         if (!__any_sync(kFull, alive)) break;
       }
     }
     if (kfull != max_iter && n == kfull && __any_sync(kFull, alive)) {
-      for (; n < max_iter; ++n) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
+      for (; n < max_iter; ++n) It::step(x, y, cr, ci, alive, cnt);
     }
     if (inside) {
       const int count = min(cnt, max_iter);

@@ -395,6 +395,27 @@ fr_status render_frame(bool mandel, fr_complex c, fr_window win, int32_t width, 
   return cuda_status(e);
 }
 
+template <class T, int FN, bool COLOR>
+cudaError_t launch_fn_t(const fr::Geom& g, const fr::Palette& pal, fr_complex c, cudaStream_t s) {
+  fr::CList<T, 1> cs;
+  cs.re[0] = state_of<T, true>(c.re);
+  cs.im[0] = state_of<T, true>(c.im);
+  const int64_t tiles = (int64_t)g.tiles_x * ((g.rows + fr::kTileH - 1) / fr::kTileH);
+  fr::escape_tile_kernel<T, true, false, COLOR, 4, 1, FN>
+      <<<dim3((unsigned)tiles, 1, 1), fr::kThreads, 0, s>>>(g, pal, cs, 0, 1, 1);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+template <int FN>
+cudaError_t launch_fn(fr_mode mode, bool color, const fr::Geom& g, const fr::Palette& pal,
+                      fr_complex c, cudaStream_t s) {
+  const bool f64 = (mode == FR_FP64_FAST || mode == FR_FP64_STRICT);
+  if (f64) return color ? launch_fn_t<double, FN, true>(g, pal, c, s)
+                        : launch_fn_t<double, FN, false>(g, pal, c, s);
+  return color ? launch_fn_t<float, FN, true>(g, pal, c, s) : launch_fn_t<float, FN, false>(g, pal, c, s);
+}
+
 }  // namespace
 
 extern "C" {
@@ -417,6 +438,28 @@ fr_status mandelbrot_param_map(fr_window win, int32_t width, int32_t height, int
                                const fr_palette* pal, uint8_t* out_rgba, fr_stream stream) {
   return render_frame(true, fr_complex{0.0, 0.0}, win, width, height, max_iter, mode, bands,
                       out_counts, pal, out_rgba, stream);
+}
+
+fr_status julia_render_fn(fr_function fn, fr_complex c, fr_window win, int32_t width,
+                          int32_t height, int32_t max_iter, fr_mode mode, uint16_t* out_counts,
+                          const fr_palette* pal, uint8_t* out_rgba, fr_stream stream) {
+  if (fn == FR_FN_Z2)
+    return julia_render_ex(c, win, width, height, max_iter, mode, fr_bands{0, 1, 0}, out_counts,
+                           pal, out_rgba, stream);
+  fr_status st = check_frame(win, width, height, max_iter);
+  if (st != FR_OK) return st;
+  if (!mode_valid(mode) || (fn != FR_FN_Z4 && fn != FR_FN_Z4_RATIONAL)) return FR_ERR_UNSUPPORTED;
+  if (!(is_fin(c.re) && is_fin(c.im))) return FR_ERR_INVALID_ARG;
+  if (!out_counts) return FR_ERR_INVALID_ARG;
+  if ((pal != nullptr) != (out_rgba != nullptr)) return FR_ERR_INVALID_ARG;
+  fr::Palette p;
+  st = make_palette(pal, &p);
+  if (st != FR_OK) return st;
+  const fr::Geom g =
+      make_geom(win, width, height, max_iter, fr_bands{0, 1, 0}, height, out_counts, out_rgba);
+  const cudaError_t e = fn == FR_FN_Z4 ? launch_fn<1>(mode, pal != nullptr, g, p, c, stream)
+                                       : launch_fn<2>(mode, pal != nullptr, g, p, c, stream);
+  return cuda_status(e);
 }
 
 fr_status julia_render_path(const fr_complex* c_host, int32_t n_frames, fr_window win,

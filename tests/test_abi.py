@@ -144,3 +144,11 @@ def test_python_api_rejects_cpu_tensors(lib):
     import torch
     with pytest.raises(B.FractalError):
         B.julia_render(0.1 + 0.2j, (0j, 2.0, 2.0), 8, 8, 100, out=torch.empty((8, 8), dtype=torch.uint16))
+
+
+def test_function_variant_validation(lib):
+    before = lib.fr_launch_count()
+    assert lib.julia_render_fn(7, C, W, 64, 64, 100, 1, DUMMY, None, None, STREAM) == 3
+    assert lib.julia_render_fn(1, C, W, 0, 64, 100, 1, DUMMY, None, None, STREAM) == 1
+    assert lib.julia_render_fn(2, B._Complex(float("nan"), 0), W, 8, 8, 100, 1, DUMMY, None, None, STREAM) == 1
+    assert lib.fr_launch_count() == before

@@ -408,3 +408,20 @@ def test_cardioid_path_frames_strict(fr):
     for k in range(len(cs)):
         ref = oracle.julia(complex(cs[k]), win.center, win.half_w, win.half_h, w, h, 100, 32)
         np.testing.assert_array_equal(got[k], ref)
+
+
+# ------------------------------------------------------------------ NEXT-3: other maps
+@pytest.mark.parametrize("fn", ["z4", "z4_rational"])
+@pytest.mark.parametrize("case", range(12))
+def test_function_variants_bit_exact(fr, fn, case):
+    """Figure 4 family (reading c-14): GPU == oracle bit for bit, both precisions,
+    fuzzed windows, plus the Figure 4 parameter value."""
+    c, win, w, h, mi = W.fuzz_cases(12, max_side=200, seed=44)[case]
+    if case == 0:
+        c, win, w, h, mi = W.FIG4_C, W.julia_window(256, 256, span_re=3.0), 256, 256, 100
+    f = {"z4": fr.Function.Z4, "z4_rational": fr.Function.Z4_RATIONAL}[fn]
+    for prec, mode in ((32, fr.Mode.FP32_STRICT), (64, fr.Mode.FP64_STRICT), (32, fr.Mode.FP32_FAST)):
+        ref = oracle.julia_fn(fn, c, win.center, win.half_w, win.half_h, w, h, mi, prec)
+        got = fr.julia_render_fn(f, c, win, w, h, mi, mode)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(np16(got), ref)
