@@ -117,6 +117,14 @@ fr_status julia_render_path(const fr_complex* c_host, int32_t n_frames, fr_windo
                             uint16_t* out_counts, const fr_palette* pal, uint8_t* out_rgba,
                             fr_stream stream);
 
+/* As julia_render_path with uint8 counts (halves the bytes delivered to
+ * rank 0 or to the host).  Requires max_iter <= 255 (else FR_ERR_UNSUPPORTED).
+ *   out_counts8 device uint8 [n_frames][height][width] */
+fr_status julia_render_path8(const fr_complex* c_host, int32_t n_frames, fr_window win,
+                             int32_t width, int32_t height, int32_t max_iter, fr_mode mode,
+                             uint8_t* out_counts8, const fr_palette* pal, uint8_t* out_rgba,
+                             fr_stream stream);
+
 /* Mandelbrot parameter map (C from the pixel, Z_0 = 0; deep zoom P:55). */
 fr_status mandelbrot_param_map(fr_window win, int32_t width, int32_t height, int32_t max_iter,
                                fr_mode mode, fr_bands bands, uint16_t* out_counts,

@@ -77,7 +77,7 @@ STATUS = {0: "FR_OK", 1: "FR_ERR_INVALID_ARG", 2: "FR_ERR_TOO_LARGE", 3: "FR_ERR
 
 # Functions declared in include/fractal.h (checked by tests/test_abi.py).
 EXPORTS = ("julia_render", "julia_render_ex", "julia_render_path", "mandelbrot_param_map",
-           "colorize", "julia_render_fn", "fr_cardioid_path", "fr_band_local_rows", "fr_band_global_row", "fr_status_str",
+           "julia_render_path8", "colorize", "julia_render_fn", "fr_cardioid_path", "fr_band_local_rows", "fr_band_global_row", "fr_status_str",
            "fr_last_cuda_error", "fr_launch_count", "fr_version")
 
 
@@ -98,6 +98,9 @@ def load():
                                         P(_Palette), vp, vp]
         lib.julia_render_path.argtypes = [vp, i32, _Window, i32, i32, i32, st, vp, P(_Palette),
                                           vp, vp]
+        lib.julia_render_path8.argtypes = [vp, i32, _Window, i32, i32, i32, st, vp, P(_Palette),
+                                           vp, vp]
+        lib.julia_render_path8.restype = st
         lib.mandelbrot_param_map.argtypes = [_Window, i32, i32, i32, st, _Bands, vp, P(_Palette),
                                              vp, vp]
         lib.colorize.argtypes = [vp, i64, i32, P(_Palette), vp, vp]
@@ -244,7 +247,8 @@ def julia_render_ex(c: complex, win, width: int, height: int, max_iter: int = 10
 def julia_render_path(cs, win, width: int, height: int, max_iter: int = 100,
                       mode: Mode = Mode.FP32_FAST, out=None, palette=None, out_rgba=None,
                       stream=None):
-    """Julia frames along a path of C values: uint16 [n, height, width]."""
+    """Julia frames along a path of C values: uint16 [n, height, width]
+    (or uint8 when `out` is a uint8 tensor; needs max_iter <= 255)."""
     import torch
     arr = np.ascontiguousarray(np.asarray(cs, dtype=np.complex128).reshape(-1))
     n = arr.shape[0]
@@ -253,13 +257,14 @@ def julia_render_path(cs, win, width: int, height: int, max_iter: int = 100,
     pal = _PalHolder(palette) if palette is not None else None
     if pal is not None and out_rgba is None:
         out_rgba = torch.empty((n, height, width, 4), dtype=torch.uint8, device="cuda")
-    p = _dev_ptr(out, "uint16", n * width * height, "out")
+    u8 = getattr(out, "dtype", None) is not None and str(out.dtype) == "torch.uint8"
+    p = _dev_ptr(out, "uint8" if u8 else "uint16", n * width * height, "out")
     q = (_dev_ptr(out_rgba, "uint8", n * width * height * 4, "out_rgba")
          if out_rgba is not None else None)
-    rc = load().julia_render_path(ctypes.c_void_p(arr.ctypes.data), n, _window(win), width,
-                                  height, max_iter, int(mode), p,
-                                  ctypes.byref(pal.c) if pal else None, q, _stream(stream))
-    _check(rc, "julia_render_path")
+    fn = load().julia_render_path8 if u8 else load().julia_render_path
+    rc = fn(ctypes.c_void_p(arr.ctypes.data), n, _window(win), width, height, max_iter,
+            int(mode), p, ctypes.byref(pal.c) if pal else None, q, _stream(stream))
+    _check(rc, "julia_render_path8" if u8 else "julia_render_path")
     return (out, out_rgba) if pal is not None else out
 
 

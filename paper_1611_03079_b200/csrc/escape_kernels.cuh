@@ -37,6 +37,7 @@ struct Geom {
   int tiles_x;    // ceil(W / kTileW)
   int64_t frame_stride;  // rows * W
   uint16_t* counts;
+  uint8_t* counts8;  // uint8 counts instead (max_iter <= 255; static kernel only), else null
   uchar4* rgba;   // nullptr unless colour levels are fused
 };
 
@@ -468,8 +469,17 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
   const int f0 = blockIdx.y * fpc;
   const int f1 = min(f0 + fpc, n_frames);
   const int64_t stride = g.frame_stride;
-  uint16_t* outp = g.counts + (int64_t)(frame0 + f0) * stride + (int64_t)ly * g.W + px;
-  uchar4* outc = COLOR ? g.rgba + (outp - g.counts) : nullptr;
+  const int64_t pix0 = (int64_t)(frame0 + f0) * stride + (int64_t)ly * g.W + px;
+  // counts are uint16, or uint8 when g.counts8 is set (max_iter <= 255): byte addressing
+  const int es = g.counts8 ? 1 : 2;
+  char* outp = g.counts8 ? reinterpret_cast<char*>(g.counts8 + pix0)
+                         : reinterpret_cast<char*>(g.counts + pix0);
+  const int64_t bstride = stride * es;
+  uchar4* outc = COLOR ? g.rgba + pix0 : nullptr;
+  auto put = [&](char* q, int v) {
+    if (es == 2) *reinterpret_cast<uint16_t*>(q) = (uint16_t)v;
+    else *reinterpret_cast<uint8_t*>(q) = (uint8_t)v;
+  };
 
   int f = f0;
   if constexpr (FN == 0 && kAsmLoop<T, STRICT, K> && K == 4 && !MANDEL && NC > 1) {
@@ -488,14 +498,14 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
       }
       if (inside) {
         const int c1 = min(cnt, max_iter), c2 = min(cnt2, max_iter);
-        outp[0] = (uint16_t)c1;
-        outp[stride] = (uint16_t)c2;
+        put(outp, c1);
+        put(outp + bstride, c2);
         if (COLOR) {
           outc[0] = colour_of(spal, pal, c1, max_iter);
           outc[stride] = colour_of(spal, pal, c2, max_iter);
         }
       }
-      outp += 2 * stride;
+      outp += 2 * bstride;
       if (COLOR) outc += 2 * stride;
     }
   }
@@ -532,10 +542,10 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
     }
     if (inside) {
       const int count = min(cnt, max_iter);
-      *outp = (uint16_t)count;
+      put(outp, count);
       if (COLOR) *outc = colour_of(spal, pal, count, max_iter);
     }
-    outp += stride;
+    outp += bstride;
     if (COLOR) outc += stride;
   }
 }

@@ -92,6 +92,7 @@ fr::Geom make_geom(fr_window win, int32_t width, int32_t height, int32_t max_ite
   g.tiles_x = (width + fr::kTileW - 1) / fr::kTileW;
   g.frame_stride = rows * (int64_t)width;
   g.counts = counts;
+  g.counts8 = nullptr;
   g.rgba = reinterpret_cast<uchar4*>(rgba);
   return g;
 }
@@ -462,24 +463,26 @@ fr_status julia_render_fn(fr_function fn, fr_complex c, fr_window win, int32_t w
   return cuda_status(e);
 }
 
-fr_status julia_render_path(const fr_complex* c_host, int32_t n_frames, fr_window win,
-                            int32_t width, int32_t height, int32_t max_iter, fr_mode mode,
-                            uint16_t* out_counts, const fr_palette* pal, uint8_t* out_rgba,
-                            fr_stream stream) {
+static fr_status render_path_impl(const fr_complex* c_host, int32_t n_frames, fr_window win,
+                                  int32_t width, int32_t height, int32_t max_iter, fr_mode mode,
+                                  uint16_t* out16, uint8_t* out8, const fr_palette* pal,
+                                  uint8_t* out_rgba, fr_stream stream) {
   if (n_frames < 0) return FR_ERR_INVALID_ARG;
   fr_status st = check_frame(win, width, height, max_iter);
   if (st != FR_OK) return st;
   if (!mode_valid(mode)) return FR_ERR_UNSUPPORTED;
+  if (out8 && max_iter > 255) return FR_ERR_UNSUPPORTED;
   if (n_frames == 0) return FR_OK;
-  if (!c_host || !out_counts) return FR_ERR_INVALID_ARG;
+  if (!c_host || (!out16 && !out8)) return FR_ERR_INVALID_ARG;
   if ((pal != nullptr) != (out_rgba != nullptr)) return FR_ERR_INVALID_ARG;
   for (int32_t k = 0; k < n_frames; ++k)
     if (!(is_fin(c_host[k].re) && is_fin(c_host[k].im))) return FR_ERR_INVALID_ARG;
   fr::Palette p;
   st = make_palette(pal, &p);
   if (st != FR_OK) return st;
-  const fr::Geom g = make_geom(win, width, height, max_iter, fr_bands{0, 1, 0}, height,
-                               out_counts, out_rgba);
+  fr::Geom g = make_geom(win, width, height, max_iter, fr_bands{0, 1, 0}, height, out16,
+                         out_rgba);
+  g.counts8 = out8;
   cudaError_t e = cudaSuccess;
   for (int32_t f0 = 0; f0 < n_frames && e == cudaSuccess; f0 += fr::kMaxPathChunk) {
     const int nf = n_frames - f0 < fr::kMaxPathChunk ? n_frames - f0 : fr::kMaxPathChunk;
@@ -487,6 +490,24 @@ fr_status julia_render_path(const fr_complex* c_host, int32_t n_frames, fr_windo
                                                stream);
   }
   return cuda_status(e);
+}
+
+fr_status julia_render_path(const fr_complex* c_host, int32_t n_frames, fr_window win,
+                            int32_t width, int32_t height, int32_t max_iter, fr_mode mode,
+                            uint16_t* out_counts, const fr_palette* pal, uint8_t* out_rgba,
+                            fr_stream stream) {
+  if (n_frames > 0 && !out_counts) return FR_ERR_INVALID_ARG;
+  return render_path_impl(c_host, n_frames, win, width, height, max_iter, mode, out_counts,
+                          nullptr, pal, out_rgba, stream);
+}
+
+fr_status julia_render_path8(const fr_complex* c_host, int32_t n_frames, fr_window win,
+                             int32_t width, int32_t height, int32_t max_iter, fr_mode mode,
+                             uint8_t* out_counts8, const fr_palette* pal, uint8_t* out_rgba,
+                             fr_stream stream) {
+  if (n_frames > 0 && !out_counts8) return FR_ERR_INVALID_ARG;
+  return render_path_impl(c_host, n_frames, win, width, height, max_iter, mode, nullptr,
+                          out_counts8, pal, out_rgba, stream);
 }
 
 fr_status colorize(const uint16_t* counts, int64_t n_pixels, int32_t max_iter,

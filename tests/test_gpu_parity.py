@@ -425,3 +425,19 @@ def test_function_variants_bit_exact(fr, fn, case):
         got = fr.julia_render_fn(f, c, win, w, h, mi, mode)
         torch.cuda.synchronize()
         np.testing.assert_array_equal(np16(got), ref)
+
+
+def test_path_uint8_counts(fr):
+    """julia_render_path8: the same counts as uint8 (max_iter <= 255), fast and strict."""
+    cs = W.circle_path(40)
+    w, h = 96, 54
+    win = W.julia_window(w, h)
+    for mode in (fr.Mode.FP32_FAST, fr.Mode.FP32_STRICT):
+        a = fr.julia_render_path(cs, win, w, h, 255, mode)
+        b = fr.julia_render_path(cs, win, w, h, 255, mode,
+                                 out=torch.empty((40, h, w), dtype=torch.uint8, device="cuda"))
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(np16(a), b.cpu().numpy().astype(np.uint16))
+    with pytest.raises(fr.FractalError):
+        fr.julia_render_path(cs, win, w, h, 256, fr.Mode.FP32_FAST,
+                             out=torch.empty((40, h, w), dtype=torch.uint8, device="cuda"))
