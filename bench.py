@@ -303,10 +303,14 @@ def main():
             "clocks": clocks,
             "roofline": roof,
         }
+    # ---- the exchange step (N > 1): NCCL gather of every rank's frames to rank 0
+    gather = measure_gather(out, world, rank, barrier) if world > 1 else None
     # ---- end-to-end through the public API with HOST buffers (pinned), N GPUs
     e2e = measure_e2e(fr, W, cs, win, world, args, barrier, stream)
     if rank == 0:
         line["e2e"] = e2e
+        if gather is not None:
+            line["gather_to_rank0"] = gather
         if world == 1:
             line["cpu_baseline"] = cpu_oracle_rate(cs, seconds=args.cpu_seconds)
             if not args.no_extra:
@@ -316,6 +320,37 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def measure_gather(out, world, rank, barrier):
+    """Time the delivery of all ranks' frames to rank 0 (torch.distributed.gather over
+    NCCL; paper_1611_03079_b200.distributed.gather_padded), max over ranks.  Reported
+    beside, not inside, the compute-resident `value`."""
+    import torch
+    import torch.distributed as dist
+    from paper_1611_03079_b200 import distributed as D
+    try:
+        reps = 2
+        D.gather_padded(out, out.shape[0], 0)  # warm-up (NCCL communicator set-up)
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(reps):
+            parts = D.gather_padded(out, out.shape[0], 0)
+            del parts
+        t1.record()
+        barrier()
+        ms = t0.elapsed_time(t1) / reps
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        nbytes = out.numel() * out.element_size() * (world - 1)
+        return {"ms": ms, "bytes_into_rank0": nbytes, "GB_per_s": nbytes / (ms * 1e-3) / 1e9,
+                "note": "uint16 frames of ranks 1..N-1 to rank 0 (NCCL gather, uint8 view); "
+                        "the rank-0 ingress bound is ~0.77-0.9 TB/s (B200_PROFILING.md)"}
+    except Exception as e:  # report, never fail the bench line
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
 
 
 def measure_e2e(fr, W, cs, win, world, args, barrier, stream):
