@@ -101,7 +101,8 @@ fr_status julia_render(fr_complex c, fr_window win, int32_t width, int32_t heigh
                        int32_t max_iter, uint16_t* out_counts, fr_stream stream);
 
 /* Julia frame with explicit mode, cyclic bands and optional fused colour levels.
- *   out_counts device uint16 [fr_band_local_rows(height, bands)][width]
+ *   out_counts device uint16 [fr_band_local_rows(height, bands)][width]; a rank that holds
+ *              no band (0 local rows) is a no-op returning FR_OK, null pointers allowed
  *   pal        NULL, or a palette (then out_rgba is required: device uint8 [rows][width][4]) */
 fr_status julia_render_ex(fr_complex c, fr_window win, int32_t width, int32_t height,
                           int32_t max_iter, fr_mode mode, fr_bands bands, uint16_t* out_counts,

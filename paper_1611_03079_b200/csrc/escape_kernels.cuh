@@ -438,21 +438,11 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
                    int n_frames, int fpc) {
   static_assert(FN == 0 || (STRICT && !MANDEL), "map variants: strict Julia frames");
   __shared__ uchar4 spal[COLOR ? 256 : 1];
-  __shared__ T sre[kTileW];
-  __shared__ T sim[kTileH];
   const int tile = blockIdx.x;
   const int ty = tile / g.tiles_x;
   const int tx = tile - ty * g.tiles_x;
-  {
-    const int t = threadIdx.x;
-    if (t < kTileW) {
-      const int px = min(tx * kTileW + t, g.W - 1);
-      sre[t] = to_state<T, STRICT>(pixel_re(g, px));
-    } else if (t < kTileW + kTileH) {
-      const int ly = min(ty * kTileH + (t - kTileW), g.rows - 1);
-      sim[t - kTileW] = to_state<T, STRICT>(pixel_im(g, global_row(g, ly)));
-    }
-    if (COLOR) spal[t] = pal.e[t];
+  if (COLOR) {
+    spal[threadIdx.x] = pal.e[threadIdx.x];
     __syncthreads();
   }
   const int lane = threadIdx.x & 31;
@@ -462,8 +452,10 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
   const int px = tx * kTileW + cx;
   const int ly = ty * kTileH + cy;
   const bool inside = (px < g.W) && (ly < g.rows);
-  const T are = sre[cx];
-  const T aim = sim[cy];
+  // this thread's pixel in the plane (binary64 map, one rounding to T); no CTA barrier:
+  // the cost is amortised over the frame group
+  const T are = to_state<T, STRICT>(pixel_re(g, min(px, g.W - 1)));
+  const T aim = to_state<T, STRICT>(pixel_im(g, global_row(g, min(ly, g.rows - 1))));
   const int max_iter = g.max_iter;
   const int kfull = max_iter - max_iter % K;  // iterations run in whole K-blocks
   const int f0 = blockIdx.y * fpc;

@@ -107,13 +107,19 @@ int static_k() {
   }
   return k;
 }
-constexpr int kFramesPerCta = 16;  // frames of a path chunk rendered per CTA (static kernel)
+constexpr int kFramesPerCta = 32;  // frames of a path chunk rendered per CTA (static kernel); FRACTAL_FPC overrides
 
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int NC>
 cudaError_t launch_tiles_t(const fr::Geom& g, const fr::Palette& pal, const fr::CList<T, NC>& cs,
                            int n_frames, int frame0, cudaStream_t s) {
   const int64_t tiles = (int64_t)g.tiles_x * ((g.rows + fr::kTileH - 1) / fr::kTileH);
-  const int fpc = n_frames < kFramesPerCta ? n_frames : kFramesPerCta;
+  static int fpc_env = -1;
+  if (fpc_env < 0) {
+    const char* ev = std::getenv("FRACTAL_FPC");
+    fpc_env = ev ? std::atoi(ev) : 0;
+  }
+  const int fpc_want = fpc_env > 0 ? fpc_env : kFramesPerCta;
+  const int fpc = n_frames < fpc_want ? n_frames : fpc_want;
   dim3 grid((unsigned)tiles, (unsigned)((n_frames + fpc - 1) / fpc), 1);
   if (sizeof(T) == 4 && !STRICT && static_k() == 2)
     fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, 2, NC>
@@ -361,14 +367,14 @@ fr_status render_frame(bool mandel, fr_complex c, fr_window win, int32_t width, 
   if (st != FR_OK) return st;
   if (!mode_valid(mode)) return FR_ERR_UNSUPPORTED;
   if (!mandel && !(is_fin(c.re) && is_fin(c.im))) return FR_ERR_INVALID_ARG;
-  if (!out_counts) return FR_ERR_INVALID_ARG;
-  if ((pal != nullptr) != (out_rgba != nullptr)) return FR_ERR_INVALID_ARG;
   const int64_t rows = local_rows(height, bands);
   if (rows < 0) return FR_ERR_INVALID_ARG;
   fr::Palette p;
   st = make_palette(pal, &p);
   if (st != FR_OK) return st;
-  if (rows == 0) return FR_OK;  // this rank holds no band
+  if (rows == 0) return FR_OK;  // this rank holds no band: nothing to write (null ok)
+  if (!out_counts) return FR_ERR_INVALID_ARG;
+  if ((pal != nullptr) != (out_rgba != nullptr)) return FR_ERR_INVALID_ARG;
   const fr::Geom g = make_geom(win, width, height, max_iter, bands, rows, out_counts, out_rgba);
   cudaError_t e;
   const Sched sched = choose_sched(mandel, c, win, max_iter);

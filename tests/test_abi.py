@@ -152,3 +152,13 @@ def test_function_variant_validation(lib):
     assert lib.julia_render_fn(1, C, W, 0, 64, 100, 1, DUMMY, None, None, STREAM) == 1
     assert lib.julia_render_fn(2, B._Complex(float("nan"), 0), W, 8, 8, 100, 1, DUMMY, None, None, STREAM) == 1
     assert lib.fr_launch_count() == before
+
+
+def test_rank_without_bands_is_a_noop(lib):
+    """A rank whose cyclic bands are all past the last row holds 0 rows: FR_OK, nothing
+    launched, null outputs accepted (an empty torch tensor has a null data_ptr)."""
+    before = lib.fr_launch_count()
+    assert B.band_local_rows(1, B.Bands(4, 3, 1)) == 0
+    assert lib.julia_render_ex(C, W, 64, 1, 100, 0, B._Bands(4, 3, 1), None, None, None, STREAM) == 0
+    assert lib.mandelbrot_param_map(W, 64, 4, 100, 2, B._Bands(4, 2, 1), None, None, None, STREAM) == 0
+    assert lib.fr_launch_count() == before

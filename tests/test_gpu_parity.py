@@ -441,3 +441,63 @@ def test_path_uint8_counts(fr):
     with pytest.raises(fr.FractalError):
         fr.julia_render_path(cs, win, w, h, 256, fr.Mode.FP32_FAST,
                              out=torch.empty((40, h, w), dtype=torch.uint8, device="cuda"))
+
+
+# ------------------------------------------------------------------ write extents (canaries)
+def _guarded(n, dtype, guard=256):
+    """A buffer with `guard` canary elements on both sides; returns (full, view)."""
+    full = torch.full((n + 2 * guard,), -1 if dtype == torch.int16 else 0xAB,
+                      dtype=dtype, device="cuda")
+    return full, full[guard:guard + n]
+
+
+def _check_canaries(full, n, dtype, guard=256):
+    a = full.cpu().numpy()
+    fill = -1 if dtype == torch.int16 else 0xAB
+    assert (a[:guard] == fill).all(), "write before the output"
+    assert (a[guard + n:] == fill).all(), "write past the output"
+    return a[guard:guard + n]
+
+
+@pytest.mark.parametrize("size", [(37, 5), (65, 17), (1, 1), (100, 33)])
+def test_outputs_written_exactly_in_bounds(fr, size):
+    """Every kernel family writes every output element exactly within its buffer: counts,
+    rgba, bands, paths (uint16 and uint8), map variants, standalone colorize.  (Stands in
+    for compute-sanitizer, which is closed on this pool.)"""
+    w, h = size
+    win = W.julia_window(w, h)
+    pal = W.palette("fire")
+    for mi in (50, 300, 1200):  # static / refill / amortised (Mandelbrot) dispatch
+        for kind in ("julia", "mandelbrot"):
+            for bands in (fr.FULL_FRAME, fr.Bands(4, 3, 1)):
+                rows = fr.band_local_rows(h, bands)
+                fc, vc = _guarded(rows * w, torch.int16)
+                fr_, vr = _guarded(rows * w * 4, torch.uint8)
+                cnt = vc.view(torch.uint16)
+                if kind == "julia":
+                    fr.julia_render_ex(0.285 + 0.01j, win, w, h, mi, fr.Mode.FP32_FAST, bands,
+                                       out=cnt, palette=pal, out_rgba=vr)
+                else:
+                    fr.mandelbrot_param_map((-0.5 + 0j, 1.5, 1.5 * h / w), w, h, mi,
+                                            fr.Mode.FP64_FAST, bands, out=cnt, palette=pal,
+                                            out_rgba=vr)
+                torch.cuda.synchronize()
+                body = _check_canaries(fc, rows * w, torch.int16)
+                assert (body != -1).all()
+                _check_canaries(fr_, rows * w * 4, torch.uint8)
+    n = 3
+    fc, vc = _guarded(n * h * w, torch.int16)
+    fr.julia_render_path(W.circle_path(n), win, w, h, 100, fr.Mode.FP32_FAST, out=vc.view(torch.uint16))
+    fb, vb = _guarded(n * h * w, torch.uint8)
+    fr.julia_render_path(W.circle_path(n), win, w, h, 100, fr.Mode.FP32_FAST, out=vb)
+    ff, vf = _guarded(h * w, torch.int16)
+    fr.julia_render_fn(fr.Function.Z4_RATIONAL, W.FIG4_C, win, w, h, 100, fr.Mode.FP32_STRICT,
+                       out=vf.view(torch.uint16))
+    counts = torch.randint(0, 300, (h * w,), dtype=torch.int32).to(torch.int16).cuda().view(torch.uint16)
+    fz, vz = _guarded(h * w * 4, torch.uint8)
+    fr.colorize(counts, 299, pal, out_rgba=vz)
+    torch.cuda.synchronize()
+    assert (_check_canaries(fc, n * h * w, torch.int16) != -1).all()
+    _check_canaries(fb, n * h * w, torch.uint8)
+    assert (_check_canaries(ff, h * w, torch.int16) != -1).all()
+    _check_canaries(fz, h * w * 4, torch.uint8)
