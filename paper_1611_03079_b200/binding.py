@@ -148,6 +148,9 @@ def _window(win) -> _Window:
 def _stream(stream):
     if stream is None:
         import torch
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        if raw is not None:  # no Stream object per call (host overhead of small frames)
+            return ctypes.c_void_p(raw(torch.cuda.current_device()))
         return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     if hasattr(stream, "cuda_stream"):
         return ctypes.c_void_p(stream.cuda_stream)
@@ -168,10 +171,27 @@ def _dev_ptr(t, dtype_name: str, numel: int, what: str):
     return ctypes.c_void_p(t.data_ptr())
 
 
+_PAL_CACHE = {}
+
+
+def _pal(palette):
+    """Host palette struct, cached per (entries, interior) object pair."""
+    key = (id(palette[0]), id(palette[1]))
+    hit = _PAL_CACHE.get(key)
+    if hit is not None and hit.src[0] is palette[0] and hit.src[1] is palette[1]:
+        return hit
+    h = _PalHolder(palette)
+    if len(_PAL_CACHE) > 64:
+        _PAL_CACHE.clear()
+    _PAL_CACHE[key] = h
+    return h
+
+
 class _PalHolder:
     """Keeps the host palette buffer alive for the duration of a call."""
 
     def __init__(self, palette):
+        self.src = palette
         entries, interior = palette
         ent = np.ascontiguousarray(np.asarray(entries, dtype=np.uint8).reshape(-1, 4))
         inter = np.asarray(interior, dtype=np.uint8).reshape(4)
@@ -229,10 +249,10 @@ def julia_render_ex(c: complex, win, width: int, height: int, max_iter: int = 10
                     palette=None, out_rgba=None, stream=None):
     """Julia frame with mode, cyclic bands and optional fused colour levels."""
     import torch
-    rows = band_local_rows(height, bands)
+    rows = height if bands is FULL_FRAME else band_local_rows(height, bands)
     if out is None:
         out = torch.empty((rows, width), dtype=torch.uint16, device="cuda")
-    pal = _PalHolder(palette) if palette is not None else None
+    pal = _pal(palette) if palette is not None else None
     if pal is not None and out_rgba is None:
         out_rgba = torch.empty((rows, width, 4), dtype=torch.uint8, device="cuda")
     p = _dev_ptr(out, "uint16", rows * width, "out")
@@ -254,7 +274,7 @@ def julia_render_path(cs, win, width: int, height: int, max_iter: int = 100,
     n = arr.shape[0]
     if out is None:
         out = torch.empty((n, height, width), dtype=torch.uint16, device="cuda")
-    pal = _PalHolder(palette) if palette is not None else None
+    pal = _pal(palette) if palette is not None else None
     if pal is not None and out_rgba is None:
         out_rgba = torch.empty((n, height, width, 4), dtype=torch.uint8, device="cuda")
     u8 = getattr(out, "dtype", None) is not None and str(out.dtype) == "torch.uint8"
@@ -273,10 +293,10 @@ def mandelbrot_param_map(win, width: int, height: int, max_iter: int = 100,
                          palette=None, out_rgba=None, stream=None):
     """Mandelbrot parameter map: C from the pixel, Z_0 = 0."""
     import torch
-    rows = band_local_rows(height, bands)
+    rows = height if bands is FULL_FRAME else band_local_rows(height, bands)
     if out is None:
         out = torch.empty((rows, width), dtype=torch.uint16, device="cuda")
-    pal = _PalHolder(palette) if palette is not None else None
+    pal = _pal(palette) if palette is not None else None
     if pal is not None and out_rgba is None:
         out_rgba = torch.empty((rows, width, 4), dtype=torch.uint8, device="cuda")
     p = _dev_ptr(out, "uint16", rows * width, "out")
@@ -293,7 +313,7 @@ def colorize(counts, max_iter: int, palette, out_rgba=None, stream=None):
     n = counts.numel()
     if out_rgba is None:
         out_rgba = torch.empty(tuple(counts.shape) + (4,), dtype=torch.uint8, device=counts.device)
-    pal = _PalHolder(palette)
+    pal = _pal(palette)
     p = _dev_ptr(counts, "uint16", n, "counts")
     q = _dev_ptr(out_rgba, "uint8", 4 * n, "out_rgba")
     rc = load().colorize(p, n, max_iter, ctypes.byref(pal.c), q, _stream(stream))
@@ -308,7 +328,7 @@ def julia_render_fn(fn, c: complex, win, width: int, height: int, max_iter: int 
     import torch
     if out is None:
         out = torch.empty((height, width), dtype=torch.uint16, device="cuda")
-    pal = _PalHolder(palette) if palette is not None else None
+    pal = _pal(palette) if palette is not None else None
     if pal is not None and out_rgba is None:
         out_rgba = torch.empty((height, width, 4), dtype=torch.uint8, device="cuda")
     p = _dev_ptr(out, "uint16", height * width, "out")

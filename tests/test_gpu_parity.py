@@ -392,7 +392,9 @@ def test_side_stream_and_launch_count(fr):
     s.synchronize()
     b = gpu_julia(fr, cfg.c, cfg.window, 64, 64, 100, fr.Mode.FP32_STRICT)
     np.testing.assert_array_equal(np16(a), b)
-    assert fr.launch_count() == before + 2
+    # one launch per render for the static kernel; the refill path may add a pre-pass
+    # and a continuation launch (FRACTAL_SCHED forced in the scheduler runs)
+    assert 2 <= fr.launch_count() - before <= 6
 
 
 # ------------------------------------------------------------------ NEXT-2: cardioid path
