@@ -315,7 +315,14 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
       e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       g_launches.fetch_add(1, std::memory_order_relaxed);
-      const unsigned blocks2 = (unsigned)sm_count();
+      static int c2 = -1;  // continuation CTAs per SM (FRACTAL_CONT_CTAS, default 2)
+      if (c2 < 0) {
+        const char* ev = std::getenv("FRACTAL_CONT_CTAS");
+        c2 = ev ? std::atoi(ev) : 2;
+        if (c2 < 1) c2 = 1;
+        if (c2 > occ) c2 = occ;
+      }
+      const unsigned blocks2 = (unsigned)(sm_count() * c2);
       kern<<<blocks2, fr::kThreads, 0, s>>>(g, pal, jcr, jci, ws, (unsigned)slots, 0u, cont,
                                             fr::kContinue);
     } else {
