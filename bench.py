@@ -447,6 +447,28 @@ def extras(fr, W, torch):
         b.synchronize()
         ms = a.elapsed_time(b) / reps
         s = int((out.view(torch.int16).to(torch.int64) & 0xFFFF).sum().item())
+        ms_graph = None
+        if name == "cfg2":  # CUDA graph of 50 frames: no launch gaps between frames
+            try:
+                g = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    fn()
+                torch.cuda.current_stream().wait_stream(side)
+                with torch.cuda.graph(g):
+                    for _ in range(50):
+                        fn()
+                g.replay()
+                torch.cuda.synchronize()
+                a.record()
+                for _ in range(4):
+                    g.replay()
+                b.record()
+                b.synchronize()
+                ms_graph = a.elapsed_time(b) / 200
+            except Exception as e:  # report, never fail the line
+                ms_graph = f"graph capture failed: {type(e).__name__}"
         lanes = FP64_LANES_PER_SM if prec == 64 else FP32_LANES_PER_SM
         peak = SM_COUNT * lanes * f_max * 1e6 / ALG_OPS_PER_ITER / 1e9
         res[name] = {"ms": ms, "gpix_iter_s": s / (ms * 1e-3) / 1e9, "pixel_iters": s,
@@ -455,6 +477,11 @@ def extras(fr, W, torch):
                      / ALG_OPS_PER_ITER, "mode": mode.name,
                      "fused_colorize": bool(pal), "reps": reps,
                      "note": "back-to-back launches, CUDA events"}
+        if ms_graph is not None:
+            res[name]["ms_cuda_graph"] = ms_graph
+            if isinstance(ms_graph, float):
+                res[name]["gpix_iter_s_cuda_graph"] = s / (ms_graph * 1e-3) / 1e9
+                res[name]["frames_per_s_cuda_graph"] = 1e3 / ms_graph
         del out, rgba
     torch.cuda.empty_cache()
     return res

@@ -1,0 +1,64 @@
+"""The multi-GPU code path on the one GPU available: an NCCL process group of world
+size 1 runs render_path_sharded / render_bands (partition + torch.distributed.gather
+over NCCL with uint8 views) and must reproduce the single-call renders byte for byte.
+World sizes > 1 are covered on CPU with gloo (tests/test_distributed.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def nccl():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.distributed as dist
+    store = dist.TCPStore("127.0.0.1", _port(), 1, True)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+def _np16(t):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def test_render_path_sharded_nccl(nccl):
+    from paper_1611_03079_b200 import binding as fr
+    from paper_1611_03079_b200 import distributed as D
+    from paper_1611_03079_b200 import workloads as W
+    cs = W.circle_path(24)
+    win = W.julia_window(320, 180)
+    full = D.render_path_sharded(cs, win, 320, 180, 100, fr.Mode.FP32_STRICT)
+    ref = fr.julia_render_path(cs, win, 320, 180, 100, fr.Mode.FP32_STRICT)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_np16(full), _np16(ref))
+
+
+@pytest.mark.parametrize("kind", ["julia", "mandelbrot"])
+def test_render_bands_nccl(nccl, kind):
+    from paper_1611_03079_b200 import binding as fr
+    from paper_1611_03079_b200 import distributed as D
+    from paper_1611_03079_b200 import workloads as W
+    w, h = 480, 270
+    win = W.julia_window(w, h) if kind == "julia" else W.mandel_window(w, h)
+    img = D.render_bands(kind, win, w, h, 300, 15, c=-0.7269 + 0.1889j)
+    if kind == "julia":
+        ref = fr.julia_render_ex(-0.7269 + 0.1889j, win, w, h, 300, fr.Mode.FP32_FAST)
+    else:
+        ref = fr.mandelbrot_param_map(win, w, h, 300, fr.Mode.FP64_FAST)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_np16(img), _np16(ref))
