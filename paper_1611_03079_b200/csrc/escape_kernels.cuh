@@ -418,6 +418,30 @@ __device__ __forceinline__ int fast_vote_loop2_f32<4>(float& x, float& y, int& c
       : "r"(kfull), "r"(0), "r"(0), "f"(cr2), "f"(ci2), "f"(cr2b), "f"(ci2b));
   return n;
 }
+template <>
+__device__ __forceinline__ int fast_vote_loop2_f32<2>(float& x, float& y, int& cnt,
+                                                      unsigned& alive, float& x2, float& y2,
+                                                      int& cnt2, unsigned& alive2, float cr2,
+                                                      float ci2, float cr2b, float ci2b,
+                                                      int kfull) {
+  int n;
+  asm volatile(
+      "{\n\t.reg .pred pa, pb, pm;\n\t.reg .f32 yy, m, t, yy2, m2, t2;\n\t"
+      "setp.ne.u32 pa, %3, 0;\n\tsetp.ne.u32 pb, %8, 0;\n\tmov.u32 %4, 0;\n\t"
+      "setp.gt.s32 pm, %9, 0;\n\t@!pm bra FR_K2B_DONE;\n"
+      "FR_K2B_LOOP:\n\t" FR_FAST_STEP2 FR_FAST_STEP2
+      "add.s32 %4, %4, 2;\n\t"
+      "or.pred pm, pa, pb;\n\t"
+      "vote.sync.any.pred pm, pm, 0xffffffff;\n\t"
+      "setp.lt.and.s32 pm, %4, %9, pm;\n\t"
+      "@pm bra FR_K2B_LOOP;\n"
+      "FR_K2B_DONE:\n\t"
+      "selp.u32 %3, 1, 0, pa;\n\tselp.u32 %8, 1, 0, pb;\n\t}"
+      : "+f"(x), "+f"(y), "+r"(cnt), "+r"(alive), "=r"(n), "+f"(x2), "+f"(y2), "+r"(cnt2),
+        "+r"(alive2)
+      : "r"(kfull), "r"(0), "r"(0), "f"(cr2), "f"(ci2), "f"(cr2b), "f"(ci2b));
+  return n;
+}
 #undef FR_FAST_STEP2
 
 template <class T, bool STRICT, int K>
@@ -474,13 +498,13 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
   };
 
   int f = f0;
-  if constexpr (FN == 0 && kAsmLoop<T, STRICT, K> && K == 4 && !MANDEL && NC > 1) {
+  if constexpr (FN == 0 && kAsmLoop<T, STRICT, K> && !MANDEL && NC > 1) {
     // two frames per lane (ILP); the remaining odd frame goes through the loop below
     for (; f + 1 < f1; f += 2) {
       float x = are, y = aim, x2 = are, y2 = aim;
       unsigned alive = inside ? 1u : 0u, alive2 = alive;
       int cnt = 0, cnt2 = 0;
-      int n = fast_vote_loop2_f32<4>(x, y, cnt, alive, x2, y2, cnt2, alive2, cs.re[f], cs.im[f],
+      int n = fast_vote_loop2_f32<K>(x, y, cnt, alive, x2, y2, cnt2, alive2, cs.re[f], cs.im[f],
                                      cs.re[f + 1], cs.im[f + 1], kfull);
       if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
         for (; n < max_iter; ++n) {
