@@ -484,7 +484,35 @@ def extras(fr, W, torch):
                 res[name]["frames_per_s_cuda_graph"] = 1e3 / ms_graph
         del out, rgba
     torch.cuda.empty_cache()
+    res["colorize_hbm"] = colorize_bandwidth(fr, W, torch)
     return res
+
+
+def colorize_bandwidth(fr, W, torch):
+    """Standalone colour levels (N6) on 512 frames of 1080p counts (2.1 GB read + 4.2 GB
+    written, >> L2): algorithmic bytes / time against the measured HBM copy peak."""
+    peaks = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6556.2))
+    n = 512 * W_PX * H_PX
+    counts = torch.randint(0, 101, (n,), dtype=torch.int32, device="cuda").to(torch.int16).view(torch.uint16)
+    rgba = torch.empty((n, 4), dtype=torch.uint8, device="cuda")
+    pal = W.palette("classic")
+    fr.colorize(counts, 100, pal, out_rgba=rgba)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(5):
+        fr.colorize(counts, 100, pal, out_rgba=rgba)
+    b.record()
+    b.synchronize()
+    ms = a.elapsed_time(b) / 5
+    gbs = n * 6 / (ms * 1e-3) / 1e9
+    del counts, rgba
+    torch.cuda.empty_cache()
+    return {"pixels": n, "ms": ms, "GB_per_s": gbs, "peak_GB_per_s": hbm, "frac": gbs / hbm,
+            "bound": "hbm", "bytes_per_pixel": 6,
+            "peak_basis": "MEASURED_PEAKS.json hbm_gbs (torch copy, read+write)"}
 
 
 if __name__ == "__main__":

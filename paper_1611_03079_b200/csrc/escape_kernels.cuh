@@ -745,19 +745,12 @@ escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
       const int thr = exhausted ? 1 : (TH < n_held ? TH : n_held);
       const int lim = held ? max_iter : 0x7fffffff;  // lanes without a pixel never finish
       if (!held) alive = 0u;
-      // ... or once the finished lanes have idled long enough: an event costs about as
-      // much as kIdleBudget lane-blocks of idling (one block of K iterations is
-      // ~(7K+6)/32 warp-instructions per lane; an event ~40)
-      constexpr int kIdleBudget = (40 * 32) / (7 * K + 6) + 1;
-      int idle = 0;
       for (;;) {
 #pragma unroll
         for (int j = 0; j < K; ++j) It::step(x, y, cr, ci, alive, cnt);
         fin = held && (!alive || cnt >= lim);
         fm = __ballot_sync(kFull, fin);
-        const int nf = __popc(fm);
-        idle += nf;
-        if (nf >= thr || idle >= kIdleBudget) break;
+        if (__popc(fm) >= thr) break;
       }
     } else {
       // a finished lane freezes (x0, y0, cnt) until the warp services it

@@ -21,6 +21,17 @@ thread_local int32_t g_last_cuda_error = 0;
 
 constexpr int64_t kMaxFramePixels = int64_t(1) << 31;  // S:182 resource limit
 
+// Tuning knobs read once from the environment (thread-safe: function-local statics are
+// initialised exactly once).  Defaults are the measured best settings.
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+bool env_is(const char* name, const char* value) {
+  const char* e = std::getenv(name);
+  return e && !std::strcmp(e, value);
+}
+
 inline bool is_fin(double v) { return std::isfinite(v); }
 
 fr_status cuda_status(cudaError_t e) {
@@ -100,11 +111,7 @@ fr::Geom make_geom(fr_window win, int32_t width, int32_t height, int32_t max_ite
 // iterations per vote block of the static kernel (FRACTAL_STATIC_K=2|4 for fp32 fast)
 constexpr int kStaticK = 4;
 int static_k() {
-  static int k = 0;
-  if (k == 0) {
-    const char* e = std::getenv("FRACTAL_STATIC_K");
-    k = (e && !std::strcmp(e, "2")) ? 2 : 4;
-  }
+  static const int k = env_is("FRACTAL_STATIC_K", "2") ? 2 : 4;
   return k;
 }
 constexpr int kFramesPerCta = 32;  // frames of a path chunk rendered per CTA (static kernel); FRACTAL_FPC overrides
@@ -113,11 +120,7 @@ template <class T, bool STRICT, bool MANDEL, bool COLOR, int NC>
 cudaError_t launch_tiles_t(const fr::Geom& g, const fr::Palette& pal, const fr::CList<T, NC>& cs,
                            int n_frames, int frame0, cudaStream_t s) {
   const int64_t tiles = (int64_t)g.tiles_x * ((g.rows + fr::kTileH - 1) / fr::kTileH);
-  static int fpc_env = -1;
-  if (fpc_env < 0) {
-    const char* ev = std::getenv("FRACTAL_FPC");
-    fpc_env = ev ? std::atoi(ev) : 0;
-  }
+  static const int fpc_env = env_int("FRACTAL_FPC", 0);
   const int fpc_want = fpc_env > 0 ? fpc_env : kFramesPerCta;
   const int fpc = n_frames < fpc_want ? n_frames : fpc_want;
   dim3 grid((unsigned)tiles, (unsigned)((n_frames + fpc - 1) / fpc), 1);
@@ -184,6 +187,15 @@ cudaError_t launch_tiles(fr_mode mode, bool color, const fr::Geom& g, const fr::
 std::mutex g_ws_mutex;
 std::map<std::pair<int, uintptr_t>, fr::Workspace*> g_ws;
 
+// Lazily created per-stream device buffers cannot be created while the stream is being
+// captured into a CUDA graph (cudaMalloc is not capturable): make the first call on a
+// stream outside capture (tests/bench warm up first); during capture a missing buffer
+// is reported as cudaErrorStreamCaptureUnsupported instead of breaking the capture.
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone;
+}
+
 cudaError_t workspace_for(cudaStream_t s, fr::Workspace** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -195,6 +207,7 @@ cudaError_t workspace_for(cudaStream_t s, fr::Workspace** out) {
     *out = it->second;
     return cudaSuccess;
   }
+  if (capturing(s)) return cudaErrorStreamCaptureUnsupported;
   fr::Workspace* w = nullptr;
   e = cudaMalloc(&w, sizeof(fr::Workspace));
   if (e != cudaSuccess) return e;
@@ -221,6 +234,7 @@ cudaError_t buffer_for(std::map<std::pair<int, uintptr_t>, std::pair<void*, size
     *out = it->second.first;
     return cudaSuccess;
   }
+  if (capturing(s)) return cudaErrorStreamCaptureUnsupported;
   if (it != g_cont.end()) {
     cudaStreamSynchronize(s);  // the old buffer may still be in use on this stream
     cudaFree(it->second.first);
@@ -241,22 +255,16 @@ cudaError_t cont_buffer_for(cudaStream_t s, size_t bytes, void** out) {
 // Hand-off + continuation launch for kernel R (opt-in, FRACTAL_CONT=1): measured within
 // run-to-run noise of the single-launch drain on cfg3 (0.28-0.30 ms either way).
 bool cont_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("FRACTAL_CONT");
-    v = (e && !std::strcmp(e, "1")) ? 1 : 0;
-  }
-  return v == 1;
+  static const bool v = env_is("FRACTAL_CONT", "1");
+  return v;
 }
 
 int sm_count() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      sms <= 0)
+    sms = 148;
   return sms;
 }
 
@@ -265,11 +273,7 @@ int sm_count() {
 // 0.30 vs 0.36 ms), CTA-local for long uniform counts (cfg5: 641 vs 663 ms).
 // FRACTAL_REFILL_CPC overrides.
 int refill_cpc(bool amort) {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = std::getenv("FRACTAL_REFILL_CPC");
-    v = e ? std::atoi(e) : -1;
-  }
+  static const int v = env_int("FRACTAL_REFILL_CPC", -1);
   if (v >= 0) return v;
   return amort ? 16 : 0;
 }
@@ -291,11 +295,13 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
     fr::Workspace* ws = nullptr;
     e = workspace_for(s, &ws);
     if (e != cudaSuccess) return e;
-    static int occ = 0;  // per instantiation
-    if (occ == 0) {
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, fr::kThreads, 0);
-      if (e != cudaSuccess || occ <= 0) occ = 1;
-    }
+    static const int occ = [&] {  // per instantiation, computed once
+      int o = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, fr::kThreads, 0) !=
+              cudaSuccess || o <= 0)
+        o = 1;
+      return o;
+    }();
     int64_t blocks = (int64_t)sm_count() * occ;
     const int64_t need = (n_chunks + fr::kThreads / 32 - 1) / (fr::kThreads / 32);
     if (blocks > need) blocks = need;
@@ -315,13 +321,9 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
       e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       g_launches.fetch_add(1, std::memory_order_relaxed);
-      static int c2 = -1;  // continuation CTAs per SM (FRACTAL_CONT_CTAS, default 2)
-      if (c2 < 0) {
-        const char* ev = std::getenv("FRACTAL_CONT_CTAS");
-        c2 = ev ? std::atoi(ev) : 2;
-        if (c2 < 1) c2 = 1;
-        if (c2 > occ) c2 = occ;
-      }
+      // continuation CTAs per SM (FRACTAL_CONT_CTAS, default 2)
+      static const int c2_env = env_int("FRACTAL_CONT_CTAS", 2);
+      const int c2 = c2_env < 1 ? 1 : (c2_env > occ ? occ : c2_env);
       const unsigned blocks2 = (unsigned)(sm_count() * c2);
       kern<<<blocks2, fr::kThreads, 0, s>>>(g, pal, jcr, jci, ws, (unsigned)slots, 0u, cont,
                                             fr::kContinue);
@@ -336,10 +338,9 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
 
 // Tuning variants of the refill kernel for FP32_FAST (FRACTAL_REFILL=K,TH); default 16,8.
 int refill_variant() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {
     const char* e = std::getenv("FRACTAL_REFILL");
-    v = 0;
+    int v = 0;
     if (e) {
       if (!std::strcmp(e, "8,8")) v = 1;
       else if (!std::strcmp(e, "16,16")) v = 2;
@@ -349,7 +350,8 @@ int refill_variant() {
       else if (!std::strcmp(e, "16,1")) v = 6;
       else if (!std::strcmp(e, "16,4")) v = 7;
     }
-  }
+    return v;
+  }();
   return v;
 }
 
@@ -412,14 +414,10 @@ bool monotone_ok(bool mandel, fr_complex c, fr_window w) {
 enum Sched { kStatic = 0, kRefill = 1, kAmort = 2 };
 
 Sched choose_sched(bool mandel, fr_complex c, fr_window w, int max_iter) {
-  static int forced = -2;
-  if (forced == -2) {
-    const char* e = std::getenv("FRACTAL_SCHED");
-    forced = -1;
-    if (e && !std::strcmp(e, "static")) forced = kStatic;
-    if (e && !std::strcmp(e, "refill")) forced = kRefill;
-    if (e && !std::strcmp(e, "amort")) forced = kAmort;
-  }
+  static const int forced = env_is("FRACTAL_SCHED", "static")   ? kStatic
+                            : env_is("FRACTAL_SCHED", "refill") ? kRefill
+                            : env_is("FRACTAL_SCHED", "amort")  ? kAmort
+                                                                 : -1;
   const bool mono = monotone_ok(mandel, c, w);
   if (forced >= 0) return (forced == kAmort && !mono) ? kRefill : (Sched)forced;
   if (max_iter < 256) return kStatic;
