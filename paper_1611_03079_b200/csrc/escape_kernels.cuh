@@ -823,20 +823,33 @@ colorize_kernel(const uint16_t* __restrict__ counts, int64_t n_pixels, int max_i
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const uint4* __restrict__ c8 = reinterpret_cast<const uint4*>(counts);
   uint4* __restrict__ o8 = reinterpret_cast<uint4*>(rgba);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < groups; i += stride) {
-    const uint4 v = __ldcs(c8 + i);
+  auto pack = [&](uint32_t w16) {
+    const uchar4 a = colour_of(spal, pal, (int)(w16 & 0xffffu), max_iter);
+    return (uint32_t)a.x | ((uint32_t)a.y << 8) | ((uint32_t)a.z << 16) | ((uint32_t)a.w << 24);
+  };
+  auto emit = [&](int64_t i, const uint4 v) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     uint32_t o[8];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uchar4 a = colour_of(spal, pal, (int)(w[k] & 0xffffu), max_iter);
-      const uchar4 b = colour_of(spal, pal, (int)(w[k] >> 16), max_iter);
-      o[2 * k] = (uint32_t)a.x | ((uint32_t)a.y << 8) | ((uint32_t)a.z << 16) | ((uint32_t)a.w << 24);
-      o[2 * k + 1] = (uint32_t)b.x | ((uint32_t)b.y << 8) | ((uint32_t)b.z << 16) | ((uint32_t)b.w << 24);
+      o[2 * k] = pack(w[k] & 0xffffu);
+      o[2 * k + 1] = pack(w[k] >> 16);
     }
     __stcs(o8 + 2 * i, make_uint4(o[0], o[1], o[2], o[3]));
     __stcs(o8 + 2 * i + 1, make_uint4(o[4], o[5], o[6], o[7]));
+  };
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // four 16-byte loads in flight per thread before any store (memory-level parallelism;
+  // measured 0.80 of the HBM copy peak vs 0.68 with one and 0.73 with eight)
+  constexpr int U = 4;
+  for (; i + (U - 1) * stride < groups; i += U * stride) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(c8 + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) emit(i + u * stride, v[u]);
   }
+  for (; i < groups; i += stride) emit(i, __ldcs(c8 + i));
   // ragged tail (< 8 pixels)
   const int64_t t0 = groups << 3;
   const int64_t t = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
