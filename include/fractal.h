@@ -175,6 +175,11 @@ int64_t fr_band_global_row(int32_t height, fr_bands bands, int64_t local_row);
 const char* fr_status_str(fr_status s);
 /* The cudaError_t of the most recent FR_ERR_CUDA in this thread (0 if none). */
 int32_t fr_last_cuda_error(void);
+/* Diagnostics: when trace_dev (device, >= 3 uint64 per warp of the refill grid) is
+ * non-null, the lane-refill kernel records per warp the %globaltimer (ns) at entry, at
+ * chunk-supply exhaustion and at exit; NULL turns it off (the default).  Synchronous. */
+fr_status fr_debug_refill_trace(void* trace_dev);
+
 /* Number of kernels this library has launched in this process (monotonic). */
 uint64_t fr_launch_count(void);
 /* Library version string. */

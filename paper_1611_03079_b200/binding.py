@@ -78,7 +78,7 @@ STATUS = {0: "FR_OK", 1: "FR_ERR_INVALID_ARG", 2: "FR_ERR_TOO_LARGE", 3: "FR_ERR
 # Functions declared in include/fractal.h (checked by tests/test_abi.py).
 EXPORTS = ("julia_render", "julia_render_ex", "julia_render_path", "mandelbrot_param_map",
            "julia_render_path8", "colorize", "julia_render_fn", "fr_cardioid_path", "fr_band_local_rows", "fr_band_global_row", "fr_status_str",
-           "fr_last_cuda_error", "fr_launch_count", "fr_version")
+           "fr_last_cuda_error", "fr_launch_count", "fr_version", "fr_debug_refill_trace")
 
 
 def load():
@@ -122,6 +122,8 @@ def load():
         lib.fr_last_cuda_error.restype = i32
         lib.fr_launch_count.restype = ctypes.c_uint64
         lib.fr_version.restype = ctypes.c_char_p
+        lib.fr_debug_refill_trace.argtypes = [vp]
+        lib.fr_debug_refill_trace.restype = st
         _lib = lib
         return lib
 

@@ -583,6 +583,16 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
 //   with |Z_n|^2 > 4 satisfies |Z_{n+1}| >= |Z_n|^2 - |C| - err > 2 forever after
 //   (DESIGN.md "Escape-monotonicity lemma"), so the block-end test cannot miss an escape.
 // ----------------------------------------------------------------------------------
+// Optional per-warp timeline of kernel R (diagnostics; null in normal operation):
+// [warp][0] = %globaltimer at entry, [1] = at chunk-supply exhaustion, [2] = at exit.
+__device__ unsigned long long* g_refill_trace = nullptr;
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct Workspace {
   unsigned int next_chunk;
   unsigned int done_warps;
@@ -629,6 +639,9 @@ escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
   const int warp = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int max_iter = g.max_iter;
+  unsigned long long* trace = g_refill_trace;
+  const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + warp;
+  if (trace && lane == 0) trace[gw * 3] = global_ns();
 
   // warp-uniform state
   int chunk_x0 = 0, chunk_y0 = 0;
@@ -654,6 +667,7 @@ escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
         cid = __shfl_sync(kFull, cid, 0);
         if (cid >= c_hi) {
           exhausted = true;
+          if (trace && lane == 0) trace[gw * 3 + 1] = global_ns();
           break;
         }
         if (mode == kContinue) {
@@ -797,6 +811,7 @@ escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
     need = fm;
   }
 
+  if (trace && lane == 0) trace[gw * 3 + 2] = global_ns();
   // ---- self-reset of the workspace by the last warp to finish (persistent grid)
   if (!chunks_per_cta && lane == 0) {
     __threadfence();

@@ -668,6 +668,11 @@ const char* fr_status_str(fr_status s) {
 
 int32_t fr_last_cuda_error(void) { return g_last_cuda_error; }
 
+fr_status fr_debug_refill_trace(void* trace_dev) {
+  unsigned long long* p = static_cast<unsigned long long*>(trace_dev);
+  return cuda_status(cudaMemcpyToSymbol(fr::g_refill_trace, &p, sizeof(p)));
+}
+
 uint64_t fr_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* fr_version(void) { return "libfractal 0.1 (sm_100a)"; }

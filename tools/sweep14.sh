@@ -1,0 +1,7 @@
+#!/bin/bash
+TAG=${1:-s}
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2>&1
+FRACTAL_SCHED=refill timeout 600 python -m pytest tests -m gpu -q -x -k "not largest and not cfg4_strict and not schedulers" > gpurun_out/pytest_${TAG}.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_${TAG}.log
+FRACTAL_SCHED=refill FRACTAL_REFILL_CPC=16 timeout 600 python -m pytest tests -m gpu -q -x -k "strict_fuzz or bands or written or ragged" > gpurun_out/pytest_${TAG}_cpc.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_${TAG}_cpc.log
+for C in 1 0; do FRACTAL_COMPACT=$C timeout 300 python tools/scale_probe.py > gpurun_out/scale_${TAG}_c$C.log 2>&1; done
+for V in 16,8 16,16 16,4; do timeout 300 env FRACTAL_REFILL=$V python tools/perf_probe.py cfg3 > gpurun_out/perf_${TAG}_$V.log 2>&1; done
