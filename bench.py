@@ -354,34 +354,19 @@ def measure_gather(out, world, rank, barrier):
 
 
 def measure_e2e(fr, W, cs, win, world, args, barrier, stream):
-    """Same metric end to end: per step the C values go host->device (kernel params from
-    the host array), the frames are rendered in chunks through the public API with uint8
-    counts (julia_render_path8; max_iter 100 <= 255) and every chunk's counts are copied
-    device->host into pinned memory on a second stream, overlapped with the next
-    chunk's rendering."""
+    """Same metric end to end through the C-ABI call with HOST buffers:
+    julia_render_path_host renders the rank's frames in chunks and copies every chunk's
+    uint8 counts (max_iter 100 <= 255) device->host into pinned memory on an internal
+    stream while the next chunk renders; it returns once all counts are on the host.
+    Per step: 16 B/frame of C values in (kernel parameters), 1 B/pixel of counts out."""
     import torch
     import torch.distributed as dist
     nf = len(cs)
-    chunk = 64
     host = torch.empty((nf, H_PX, W_PX), dtype=torch.uint8, pin_memory=True)
-    dev = [torch.empty((chunk, H_PX, W_PX), dtype=torch.uint8, device="cuda") for _ in range(2)]
-    copy_stream = torch.cuda.Stream()
-    done = [torch.cuda.Event() for _ in range(2)]
-    rendered = [torch.cuda.Event() for _ in range(2)]
 
     def step():
-        for j, f0 in enumerate(range(0, nf, chunk)):
-            b = j % 2
-            stream.wait_event(done[b])
-            n = min(chunk, nf - f0)
-            fr.julia_render_path(cs[f0:f0 + n], win, W_PX, H_PX, MAX_ITER, fr.Mode.FP32_FAST,
-                                 out=dev[b], stream=stream)
-            rendered[b].record(stream)
-            copy_stream.wait_event(rendered[b])
-            with torch.cuda.stream(copy_stream):
-                host[f0:f0 + n].copy_(dev[b][:n], non_blocking=True)
-            done[b].record(copy_stream)
-        stream.wait_stream(copy_stream)
+        fr.julia_render_path_host(cs, win, W_PX, H_PX, MAX_ITER, fr.Mode.FP32_FAST, out=host,
+                                  stream=stream)
 
     steps = max(2, min(args.steps, 5))
     for _ in range(2):
@@ -406,9 +391,10 @@ def measure_e2e(fr, W, cs, win, world, args, barrier, stream):
     return {"value": float(tot.item()) * steps / (ms * 1e-3) / 1e9, "unit": "Gpixel-iter/s",
             "h2d_bytes_per_step": int(nf * 16), "d2h_bytes_per_step": int(nf * H_PX * W_PX),
             "steps": steps, "ms_per_step": ms / steps,
+            "api": "julia_render_path_host (C ABI, host output buffer)",
             "note": "C values (16 B/frame) host->device as kernel parameters; uint8 counts "
-                    "(julia_render_path8) device->host into pinned memory, chunked (64 "
-                    "frames) and overlapped with rendering"}
+                    "device->host into pinned memory inside the call, 128 MiB chunks "
+                    "double-buffered and overlapped with rendering"}
 
 
 def extras(fr, W, torch):

@@ -126,6 +126,18 @@ fr_status julia_render_path8(const fr_complex* c_host, int32_t n_frames, fr_wind
                              uint8_t* out_counts8, const fr_palette* pal, uint8_t* out_rgba,
                              fr_stream stream);
 
+/* As julia_render_path, with the counts delivered to HOST memory: frames are rendered
+ * in chunks on `stream` into two device staging buffers and each chunk is copied
+ * device->host on an internal stream while the next chunk renders.  SYNCHRONOUS: returns
+ * once every count is in out_host (pinned host memory -- cudaMallocHost /
+ * cudaHostRegister -- gives overlapped copies; pageable memory works, slower).
+ *   bytes_per_count  2 (uint16) or 1 (uint8; requires max_iter <= 255)
+ *   out_host         HOST [n_frames][height][width] of bytes_per_count each
+ * Errors as julia_render_path; a bad bytes_per_count -> FR_ERR_INVALID_ARG. */
+fr_status julia_render_path_host(const fr_complex* c_host, int32_t n_frames, fr_window win,
+                                 int32_t width, int32_t height, int32_t max_iter, fr_mode mode,
+                                 int32_t bytes_per_count, void* out_host, fr_stream stream);
+
 /* Mandelbrot parameter map (C from the pixel, Z_0 = 0; deep zoom P:55). */
 fr_status mandelbrot_param_map(fr_window win, int32_t width, int32_t height, int32_t max_iter,
                                fr_mode mode, fr_bands bands, uint16_t* out_counts,

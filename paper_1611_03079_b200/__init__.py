@@ -10,7 +10,7 @@ from importlib import import_module as _imp
 
 __all__ = ["julia_render", "julia_render_ex", "julia_render_path", "mandelbrot_param_map",
            "colorize", "FractalError", "Mode", "Bands", "FULL_FRAME", "band_local_rows",
-           "band_global_row", "launch_count", "version", "cardioid_path", "julia_render_fn", "Function", "workloads"]
+           "band_global_row", "launch_count", "version", "cardioid_path", "julia_render_fn", "Function", "julia_render_path_host", "workloads"]
 
 
 def __getattr__(name):

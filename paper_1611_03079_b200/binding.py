@@ -77,7 +77,7 @@ STATUS = {0: "FR_OK", 1: "FR_ERR_INVALID_ARG", 2: "FR_ERR_TOO_LARGE", 3: "FR_ERR
 
 # Functions declared in include/fractal.h (checked by tests/test_abi.py).
 EXPORTS = ("julia_render", "julia_render_ex", "julia_render_path", "mandelbrot_param_map",
-           "julia_render_path8", "colorize", "julia_render_fn", "fr_cardioid_path", "fr_band_local_rows", "fr_band_global_row", "fr_status_str",
+           "julia_render_path8", "julia_render_path_host", "colorize", "julia_render_fn", "fr_cardioid_path", "fr_band_local_rows", "fr_band_global_row", "fr_status_str",
            "fr_last_cuda_error", "fr_launch_count", "fr_version", "fr_debug_refill_trace")
 
 
@@ -101,6 +101,8 @@ def load():
         lib.julia_render_path8.argtypes = [vp, i32, _Window, i32, i32, i32, st, vp, P(_Palette),
                                            vp, vp]
         lib.julia_render_path8.restype = st
+        lib.julia_render_path_host.argtypes = [vp, i32, _Window, i32, i32, i32, st, i32, vp, vp]
+        lib.julia_render_path_host.restype = st
         lib.mandelbrot_param_map.argtypes = [_Window, i32, i32, i32, st, _Bands, vp, P(_Palette),
                                              vp, vp]
         lib.colorize.argtypes = [vp, i64, i32, P(_Palette), vp, vp]
@@ -340,3 +342,31 @@ def julia_render_fn(fn, c: complex, win, width: int, height: int, max_iter: int 
                                 ctypes.byref(pal.c) if pal else None, q, _stream(stream))
     _check(rc, "julia_render_fn")
     return (out, out_rgba) if pal is not None else out
+
+
+def julia_render_path_host(cs, win, width: int, height: int, max_iter: int = 100,
+                           mode: Mode = Mode.FP32_FAST, out=None, stream=None):
+    """Julia frames along a C-path with the counts delivered to HOST memory (native
+    chunked render + overlapped device->host copies; synchronous).  `out`: a host
+    numpy array or CPU torch tensor of uint8 (max_iter <= 255) or uint16, shape
+    [n, height, width]; pinned torch memory gives overlapped copies."""
+    arr = np.ascontiguousarray(np.asarray(cs, dtype=np.complex128).reshape(-1))
+    n = arr.shape[0]
+    if out is None:
+        out = np.empty((n, height, width), dtype=np.uint8 if max_iter <= 255 else np.uint16)
+    if hasattr(out, "data_ptr"):  # torch CPU tensor
+        if out.is_cuda or not out.is_contiguous():
+            raise FractalError("out must be a contiguous host tensor")
+        nbytes, ptr = out.element_size(), out.data_ptr()
+        numel = out.numel()
+    else:
+        if not out.flags["C_CONTIGUOUS"]:
+            raise FractalError("out must be C-contiguous")
+        nbytes, ptr, numel = out.dtype.itemsize, out.ctypes.data, out.size
+    if nbytes not in (1, 2) or numel < n * width * height:
+        raise FractalError("out must hold n*height*width uint8/uint16 counts")
+    rc = load().julia_render_path_host(ctypes.c_void_p(arr.ctypes.data), n, _window(win), width,
+                                       height, max_iter, int(mode), nbytes, ctypes.c_void_p(ptr),
+                                       _stream(stream))
+    _check(rc, "julia_render_path_host")
+    return out

@@ -587,6 +587,82 @@ fr_status julia_render_path8(const fr_complex* c_host, int32_t n_frames, fr_wind
                           out_counts8, pal, out_rgba, stream);
 }
 
+fr_status julia_render_path_host(const fr_complex* c_host, int32_t n_frames, fr_window win,
+                                 int32_t width, int32_t height, int32_t max_iter, fr_mode mode,
+                                 int32_t bytes_per_count, void* out_host, fr_stream stream) {
+  if (n_frames < 0) return FR_ERR_INVALID_ARG;
+  if (bytes_per_count != 1 && bytes_per_count != 2) return FR_ERR_INVALID_ARG;
+  fr_status st = check_frame(win, width, height, max_iter);
+  if (st != FR_OK) return st;
+  if (!mode_valid(mode)) return FR_ERR_UNSUPPORTED;
+  if (bytes_per_count == 1 && max_iter > 255) return FR_ERR_UNSUPPORTED;
+  if (n_frames == 0) return FR_OK;
+  if (!c_host || !out_host) return FR_ERR_INVALID_ARG;
+  for (int32_t k = 0; k < n_frames; ++k)
+    if (!(is_fin(c_host[k].re) && is_fin(c_host[k].im))) return FR_ERR_INVALID_ARG;
+  const size_t frame_bytes = (size_t)width * (size_t)height * (size_t)bytes_per_count;
+  // staging: two buffers of up to 128 MiB (at least one frame each)
+  int32_t chunk = (int32_t)((size_t)(128u << 20) / frame_bytes);
+  if (chunk < 1) chunk = 1;
+  if (chunk > n_frames) chunk = n_frames;
+  cudaStream_t s = stream, cs = nullptr;
+  void* buf[2] = {nullptr, nullptr};
+  cudaEvent_t rendered[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
+  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  {
+    // stream-ordered staging from the device's default pool; keep freed staging
+    // memory in the pool between calls instead of returning it at every sync
+    static std::once_flag once;
+    std::call_once(once, [] {
+      int dev = 0;
+      cudaMemPool_t pool;
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = 1ull << 30;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+    });
+  }
+  for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+    e = cudaMallocAsync(&buf[b], frame_bytes * (size_t)chunk, s);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&rendered[b], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
+  }
+  fr_status rs = FR_OK;
+  for (int32_t f0 = 0, i = 0; f0 < n_frames && e == cudaSuccess && rs == FR_OK; f0 += chunk, ++i) {
+    const int b = i & 1;
+    const int32_t nf = n_frames - f0 < chunk ? n_frames - f0 : chunk;
+    if (i >= 2) e = cudaStreamWaitEvent(s, copied[b], 0);  // buffer b's copy is done
+    if (e != cudaSuccess) break;
+    rs = bytes_per_count == 2
+             ? render_path_impl(c_host + f0, nf, win, width, height, max_iter, mode,
+                                static_cast<uint16_t*>(buf[b]), nullptr, nullptr, nullptr,
+                                stream)
+             : render_path_impl(c_host + f0, nf, win, width, height, max_iter, mode, nullptr,
+                                static_cast<uint8_t*>(buf[b]), nullptr, nullptr, stream);
+    if (rs != FR_OK) break;
+    e = cudaEventRecord(rendered[b], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, rendered[b], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(static_cast<char*>(out_host) + (size_t)f0 * frame_bytes, buf[b],
+                          frame_bytes * (size_t)nf, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(copied[b], cs);
+  }
+  if (cs) {
+    const cudaError_t e2 = cudaStreamSynchronize(cs);
+    if (e == cudaSuccess) e = e2;
+  }
+  const cudaError_t e3 = cudaStreamSynchronize(s);  // the renders (and any fault) are done
+  if (e == cudaSuccess) e = e3;
+  for (int b = 0; b < 2; ++b) {
+    if (buf[b]) cudaFreeAsync(buf[b], s);
+    if (rendered[b]) cudaEventDestroy(rendered[b]);
+    if (copied[b]) cudaEventDestroy(copied[b]);
+  }
+  if (cs) cudaStreamDestroy(cs);
+  if (rs != FR_OK) return rs;
+  return cuda_status(e);
+}
+
 fr_status colorize(const uint16_t* counts, int64_t n_pixels, int32_t max_iter,
                    const fr_palette* pal, uint8_t* out_rgba, fr_stream stream) {
   if (n_pixels < 0 || max_iter < 1) return FR_ERR_INVALID_ARG;

@@ -503,3 +503,18 @@ def test_outputs_written_exactly_in_bounds(fr, size):
     _check_canaries(fb, n * h * w, torch.uint8)
     assert (_check_canaries(ff, h * w, torch.int16) != -1).all()
     _check_canaries(fz, h * w * 4, torch.uint8)
+
+
+def test_path_to_host_buffers(fr):
+    """julia_render_path_host: the same counts as the device path, delivered to host
+    memory (pinned and pageable, uint8 and uint16), across several staging chunks."""
+    cs = W.circle_path(70)
+    w, h = 1920, 1080
+    win = W.julia_window(w, h)
+    ref = np16(fr.julia_render_path(cs, win, w, h, 100, fr.Mode.FP32_FAST))
+    pinned = torch.empty((70, h, w), dtype=torch.uint8, pin_memory=True)
+    fr.julia_render_path_host(cs, win, w, h, 100, fr.Mode.FP32_FAST, out=pinned)
+    np.testing.assert_array_equal(pinned.numpy().astype(np.uint16), ref)
+    page16 = np.empty((70, h, w), dtype=np.uint16)
+    fr.julia_render_path_host(cs, win, w, h, 100, fr.Mode.FP32_FAST, out=page16)
+    np.testing.assert_array_equal(page16, ref)
