@@ -380,18 +380,39 @@ cudaError_t launch_refill_mode(fr_mode mode, const fr::Geom& g, const fr::Palett
   return cudaErrorInvalidValue;
 }
 
+// Kernel A variants (FRACTAL_AMORT=K,TH).  Default 64,4: measured on cfg5 (fp64 fast)
+// 592 ms; 32,4 609; 128,4 597; 64,8 601; 16,1 641-663.
+int amort_variant() {
+  static const int v = env_is("FRACTAL_AMORT", "16,1") ? 0 : env_is("FRACTAL_AMORT", "16,4") ? 1
+                       : env_is("FRACTAL_AMORT", "16,8") ? 2 : env_is("FRACTAL_AMORT", "32,1") ? 3
+                       : env_is("FRACTAL_AMORT", "32,4") ? 4 : env_is("FRACTAL_AMORT", "128,4") ? 6
+                       : env_is("FRACTAL_AMORT", "64,8") ? 7 : 5;
+  return v;
+}
+
+template <class T, bool STRICT, bool MANDEL, bool COLOR>
+cudaError_t launch_amort_t(const fr::Geom& g, const fr::Palette& pal, double2 c, cudaStream_t s) {
+  switch (amort_variant()) {
+    case 1: return launch_refill_t<T, STRICT, MANDEL, COLOR, 16, 4, true>(g, pal, c, s);
+    case 2: return launch_refill_t<T, STRICT, MANDEL, COLOR, 16, 8, true>(g, pal, c, s);
+    case 3: return launch_refill_t<T, STRICT, MANDEL, COLOR, 32, 1, true>(g, pal, c, s);
+    case 4: return launch_refill_t<T, STRICT, MANDEL, COLOR, 32, 4, true>(g, pal, c, s);
+    case 6: return launch_refill_t<T, STRICT, MANDEL, COLOR, 128, 4, true>(g, pal, c, s);
+    case 7: return launch_refill_t<T, STRICT, MANDEL, COLOR, 64, 8, true>(g, pal, c, s);
+    default: return launch_refill_t<T, STRICT, MANDEL, COLOR, 64, 4, true>(g, pal, c, s);
+    case 0: return launch_refill_t<T, STRICT, MANDEL, COLOR, 16, 1, true>(g, pal, c, s);
+    case 4: return launch_refill_t<T, STRICT, MANDEL, COLOR, 32, 4, true>(g, pal, c, s);
+  }
+}
+
 template <bool MANDEL, bool COLOR>
 cudaError_t launch_amort_mode(fr_mode mode, const fr::Geom& g, const fr::Palette& pal,
                               double2 c, cudaStream_t s) {
   switch (mode) {
-    case FR_FP32_FAST:
-      return launch_refill_t<float, false, MANDEL, COLOR, 16, 1, true>(g, pal, c, s);
-    case FR_FP32_STRICT:
-      return launch_refill_t<float, true, MANDEL, COLOR, 16, 1, true>(g, pal, c, s);
-    case FR_FP64_FAST:
-      return launch_refill_t<double, false, MANDEL, COLOR, 16, 1, true>(g, pal, c, s);
-    case FR_FP64_STRICT:
-      return launch_refill_t<double, true, MANDEL, COLOR, 16, 1, true>(g, pal, c, s);
+    case FR_FP32_FAST: return launch_amort_t<float, false, MANDEL, COLOR>(g, pal, c, s);
+    case FR_FP32_STRICT: return launch_amort_t<float, true, MANDEL, COLOR>(g, pal, c, s);
+    case FR_FP64_FAST: return launch_amort_t<double, false, MANDEL, COLOR>(g, pal, c, s);
+    case FR_FP64_STRICT: return launch_amort_t<double, true, MANDEL, COLOR>(g, pal, c, s);
   }
   return cudaErrorInvalidValue;
 }
