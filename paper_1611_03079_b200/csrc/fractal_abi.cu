@@ -399,9 +399,8 @@ cudaError_t launch_amort_t(const fr::Geom& g, const fr::Palette& pal, double2 c,
     case 4: return launch_refill_t<T, STRICT, MANDEL, COLOR, 32, 4, true>(g, pal, c, s);
     case 6: return launch_refill_t<T, STRICT, MANDEL, COLOR, 128, 4, true>(g, pal, c, s);
     case 7: return launch_refill_t<T, STRICT, MANDEL, COLOR, 64, 8, true>(g, pal, c, s);
-    default: return launch_refill_t<T, STRICT, MANDEL, COLOR, 64, 4, true>(g, pal, c, s);
     case 0: return launch_refill_t<T, STRICT, MANDEL, COLOR, 16, 1, true>(g, pal, c, s);
-    case 4: return launch_refill_t<T, STRICT, MANDEL, COLOR, 32, 4, true>(g, pal, c, s);
+    default: return launch_refill_t<T, STRICT, MANDEL, COLOR, 64, 4, true>(g, pal, c, s);
   }
 }
 
