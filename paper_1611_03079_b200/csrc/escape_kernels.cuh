@@ -567,6 +567,76 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
 }
 
 // ----------------------------------------------------------------------------------
+// Static-tile kernel for ONE frame, fast fp32, two pixels per thread (S2): CTA tile
+// 32x16, each thread iterates the pixels of rows ly and ly + 8 of its 8x4-lane warp
+// tile together in the two-orbit PTX vote loop (ILP for the FP pipe, one vote for
+// both, half the per-pixel overhead).  Julia frames share C; Mandelbrot maps take each
+// orbit's C from its pixel (Z_0 = 0).  Bit-identical to kernel S (same arithmetic).
+// ----------------------------------------------------------------------------------
+template <bool MANDEL, bool COLOR>
+__global__ void __launch_bounds__(kThreads)
+escape_tile2_kernel(const Geom g, const Palette pal, const float jcr2, const float jci2) {
+  __shared__ uchar4 spal[COLOR ? 256 : 1];
+  const int tile = blockIdx.x;
+  const int ty = tile / g.tiles_x;
+  const int tx = tile - ty * g.tiles_x;
+  if (COLOR) {
+    spal[threadIdx.x] = pal.e[threadIdx.x];
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int cx = (warp & 3) * kWarpW + (lane & 7);
+  const int cy = (warp >> 2) * kWarpH + (lane >> 3);
+  const int px = tx * kTileW + cx;
+  const int ly0 = ty * (2 * kTileH) + cy;
+  const int ly1 = ly0 + kTileH;
+  const bool in0 = (px < g.W) && (ly0 < g.rows);
+  const bool in1 = (px < g.W) && (ly1 < g.rows);
+  const float re = to_state<float, false>(pixel_re(g, min(px, g.W - 1)));
+  const float im0 = to_state<float, false>(pixel_im(g, global_row(g, min(ly0, g.rows - 1))));
+  const float im1 = to_state<float, false>(pixel_im(g, global_row(g, min(ly1, g.rows - 1))));
+  float x, y, x2, y2, cr, ci, cr2, ci2;
+  if (MANDEL) {
+    x = y = x2 = y2 = 0.0f;
+    cr = re;
+    ci = im0;
+    cr2 = re;
+    ci2 = im1;
+  } else {
+    x = re;
+    y = im0;
+    x2 = re;
+    y2 = im1;
+    cr = cr2 = jcr2;
+    ci = ci2 = jci2;
+  }
+  unsigned alive = in0 ? 1u : 0u, alive2 = in1 ? 1u : 0u;
+  int cnt = 0, cnt2 = 0;
+  const int max_iter = g.max_iter;
+  const int kfull = max_iter - max_iter % 4;
+  int n = fast_vote_loop2_f32<4>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2, kfull);
+  if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
+    for (; n < max_iter; ++n) {
+      Iter<float, false>::step(x, y, cr, ci, alive, cnt);
+      Iter<float, false>::step(x2, y2, cr2, ci2, alive2, cnt2);
+    }
+  }
+  if (in0) {
+    const int64_t off = (int64_t)ly0 * g.W + px;
+    const int c0 = min(cnt, max_iter);
+    g.counts[off] = (uint16_t)c0;
+    if (COLOR) g.rgba[off] = colour_of(spal, pal, c0, max_iter);
+  }
+  if (in1) {
+    const int64_t off = (int64_t)ly1 * g.W + px;
+    const int c1 = min(cnt2, max_iter);
+    g.counts[off] = (uint16_t)c1;
+    if (COLOR) g.rgba[off] = colour_of(spal, pal, c1, max_iter);
+  }
+}
+
+// ----------------------------------------------------------------------------------
 // Persistent lane-refill kernel (R) for one frame whose counts are heavy-tailed or long
 // (SURVEY §7 hard part 1).  Each warp owns a 32x8-pixel chunk at a time, taken from a
 // global atomic chunk counter (self-resetting workspace).  Every lane iterates its own

@@ -10,6 +10,7 @@
 #include <mutex>
 #include <new>
 #include <utility>
+#include <type_traits>
 
 #include "../../include/fractal.h"
 #include "escape_kernels.cuh"
@@ -124,6 +125,17 @@ cudaError_t launch_tiles_t(const fr::Geom& g, const fr::Palette& pal, const fr::
   const int fpc_want = fpc_env > 0 ? fpc_env : kFramesPerCta;
   const int fpc = n_frames < fpc_want ? n_frames : fpc_want;
   dim3 grid((unsigned)tiles, (unsigned)((n_frames + fpc - 1) / fpc), 1);
+  // one frame, fast fp32: two pixels per thread (kernel S2; FRACTAL_S2=0 disables)
+  static const bool s2 = !env_is("FRACTAL_S2", "0");
+  if constexpr (NC == 1 && std::is_same<T, float>::value && !STRICT) {
+    if (s2 && g.counts8 == nullptr) {
+      const int64_t tiles2 = (int64_t)g.tiles_x * ((g.rows + 2 * fr::kTileH - 1) / (2 * fr::kTileH));
+      fr::escape_tile2_kernel<MANDEL, COLOR>
+          <<<dim3((unsigned)tiles2, 1, 1), fr::kThreads, 0, s>>>(g, pal, cs.re[0], cs.im[0]);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      return cudaGetLastError();
+    }
+  }
   if (sizeof(T) == 4 && !STRICT && static_k() == 2)
     fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, 2, NC>
         <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);

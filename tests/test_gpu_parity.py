@@ -99,9 +99,9 @@ def test_strict_paper_parameters(fr, prec, c):
     np.testing.assert_array_equal(gpu_julia(fr, c, win, 256, 256, 100, strict(prec, fr)), ref)
 
 
-@pytest.mark.parametrize("case", range(48))
+@pytest.mark.parametrize("case", range(96))
 def test_strict_fuzz(fr, case):
-    c, win, w, h, mi = W.fuzz_cases(48, max_side=300)[case]
+    c, win, w, h, mi = W.fuzz_cases(96, max_side=300)[case]
     for prec in (32, 64):
         ref = oracle.julia(c, win.center, win.half_w, win.half_h, w, h, mi, prec)
         np.testing.assert_array_equal(gpu_julia(fr, c, win, w, h, mi, strict(prec, fr)), ref)
