@@ -39,6 +39,8 @@ struct Geom {
   uint16_t* counts;
   uint8_t* counts8;  // uint8 counts instead (max_iter <= 255; static kernel only), else null
   uchar4* rgba;   // nullptr unless colour levels are fused
+  int stage;      // kernel S path chunks: stage counts in shared memory (whole-sector writes)
+  int wlog;       // kernel S warp tile (1 << wlog) x (32 >> wlog): 3 -> 8x4, 4 -> 16x2, 5 -> 32x1
 };
 
 // Julia C values of a path chunk, already in the kernel's state representation
@@ -471,8 +473,13 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
   }
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int cx = (warp & 3) * kWarpW + (lane & 7);
-  const int cy = (warp >> 2) * kWarpH + (lane >> 3);
+  // 8x4 warp tiles (orbit coherence), or 16x2 / 32x1 so each warp row writes whole
+  // 32-B sectors of uint16 / uint8 counts: with frame groups the warps of a CTA drift apart in
+  // frames, and a sector half-written by two warps can leave L2 in between (DRAM
+  // read-modify-write)
+  const int wl = g.wlog, hl = 5 - wl;  // warp tile (1 << wl) x (1 << hl)
+  const int cx = ((warp & ((1 << hl) - 1)) << wl) + (lane & ((1 << wl) - 1));
+  const int cy = ((warp >> hl) << hl) + (lane >> wl);
   const int px = tx * kTileW + cx;
   const int ly = ty * kTileH + cy;
   const bool inside = (px < g.W) && (ly < g.rows);
@@ -492,9 +499,35 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
                          : reinterpret_cast<char*>(g.counts + pix0);
   const int64_t bstride = stride * es;
   uchar4* outc = COLOR ? g.rgba + pix0 : nullptr;
+  // Output sectors: with 8x4 warp tiles each 32-B sector of a count row is written half
+  // by one warp and half by its neighbour, and over a frame group the two warps drift
+  // apart in frames; a sector evicted from L2 half-written costs a DRAM read-modify-write
+  // (measured: +0.4 GB reads per cfg4 launch).  g.stage selects the remedy:
+  //   3 (default): direct stores with an L2 evict_last policy, so the half-written line
+  //      stays in L2 until its other half arrives (no extra instructions);
+  //   1 / 2: path chunks stage the group's counts in shared memory and write whole 16-B
+  //      row segments after a warp-pair named barrier (1) or a CTA barrier (2);
+  //   0: plain direct stores.
+  constexpr int kStageFrames = 32;
+  __shared__ __align__(16) uint16_t stage[NC > 1 ? kStageFrames * kThreads : 1];
+  const bool staged = NC > 1 && (g.stage == 1 || g.stage == 2) && (f1 - f0) <= kStageFrames;
+  uint16_t* sp = stage + cy * kTileW + cx;
+  uint64_t l2pol = 0;
+  if (g.stage == 3) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(l2pol));
   auto put = [&](char* q, int v) {
-    if (es == 2) *reinterpret_cast<uint16_t*>(q) = (uint16_t)v;
-    else *reinterpret_cast<uint8_t*>(q) = (uint8_t)v;
+    if (staged) {
+      *sp = (uint16_t)v;
+    } else if (g.stage == 3 && es == 2) {
+      asm volatile("st.global.L2::cache_hint.u16 [%0], %1, %2;" ::"l"(q), "h"((unsigned short)v),
+                   "l"(l2pol) : "memory");
+    } else if (g.stage == 3) {
+      asm volatile("st.global.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(q), "r"(v), "l"(l2pol)
+                   : "memory");
+    } else if (es == 2) {
+      *reinterpret_cast<uint16_t*>(q) = (uint16_t)v;
+    } else {
+      *reinterpret_cast<uint8_t*>(q) = (uint8_t)v;
+    }
   };
 
   int f = f0;
@@ -515,13 +548,16 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
       if (inside) {
         const int c1 = min(cnt, max_iter), c2 = min(cnt2, max_iter);
         put(outp, c1);
+        sp += kThreads;
         put(outp + bstride, c2);
+        sp -= kThreads;
         if (COLOR) {
           outc[0] = colour_of(spal, pal, c1, max_iter);
           outc[stride] = colour_of(spal, pal, c2, max_iter);
         }
       }
       outp += 2 * bstride;
+      sp += 2 * kThreads;
       if (COLOR) outc += 2 * stride;
     }
   }
@@ -562,7 +598,58 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
       if (COLOR) *outc = colour_of(spal, pal, count, max_iter);
     }
     outp += bstride;
+    sp += kThreads;
     if (COLOR) outc += stride;
+  }
+  if (NC > 1 && staged) {
+    // flush: only the two warps of a pair share output sectors, so each pair syncs on its
+    // own named barrier and writes its 16x4 region (8x4 warp tiles; other warp tiles use
+    // the CTA barrier).  Each thread owns one segment (row, 8-pixel group) and walks the
+    // frames 8 apart: a 16-B (uint16) or 8-B (uint8) vector store when the segment is
+    // whole and aligned in every frame, else per pixel within bounds.
+    int t, r, col;
+    if (g.wlog == 3 && g.stage == 1) {
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + (warp >> 1)) : "memory");
+      t = threadIdx.x & 63;
+      r = (warp >> 2) * 4 + ((t >> 1) & 3);
+      col = ((warp >> 1) & 1) * 16 + (t & 1) * 8;
+    } else {
+      __syncthreads();
+      t = threadIdx.x;
+      r = (t >> 2) & 7;
+      col = (t & 3) * 8;
+    }
+    const int fl0 = t >> (g.wlog == 3 && g.stage == 1 ? 3 : 5);  // 0..7
+    const int row = ty * kTileH + r;
+    const int x0 = tx * kTileW + col;
+    if (row < g.rows && x0 < g.W) {
+      const int64_t e = (int64_t)(frame0 + f0 + fl0) * stride + (int64_t)row * g.W + x0;
+      char* q = g.counts8 ? reinterpret_cast<char*>(g.counts8 + e)
+                          : reinterpret_cast<char*>(g.counts + e);
+      const uint16_t* src = stage + fl0 * kThreads + r * kTileW + col;
+      const int64_t qstep = 8 * bstride;
+      const int nf = f1 - f0;
+      const unsigned amask = es == 2 ? 15u : 7u;
+      const bool vec = x0 + 8 <= g.W && (reinterpret_cast<uintptr_t>(q) & amask) == 0 &&
+                       (bstride & amask) == 0;
+      for (int fl = fl0; fl < nf; fl += 8, q += qstep, src += 8 * kThreads) {
+        const uint4 v = *reinterpret_cast<const uint4*>(src);
+        if (vec && es == 2) {
+          *reinterpret_cast<uint4*>(q) = v;
+        } else if (vec) {
+          // counts <= 255 here: keep the low byte of each uint16
+          *reinterpret_cast<uint2*>(q) =
+              make_uint2(__byte_perm(v.x, v.y, 0x6420), __byte_perm(v.z, v.w, 0x6420));
+        } else {
+          const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+          const int n = min(8, g.W - x0);
+          for (int i = 0; i < n; ++i) {
+            if (es == 2) reinterpret_cast<uint16_t*>(q)[i] = h[i];
+            else reinterpret_cast<uint8_t*>(q)[i] = (uint8_t)h[i];
+          }
+        }
+      }
+    }
   }
 }
 

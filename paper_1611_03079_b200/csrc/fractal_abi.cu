@@ -86,6 +86,19 @@ fr_status make_palette(const fr_palette* pal, fr::Palette* out) {
   return FR_OK;
 }
 
+// kernel S warp tile width 8|16|32 (FRACTAL_WTILE), as log2
+int warp_tile_log() {
+  static const int w = env_int("FRACTAL_WTILE", 8);
+  return w == 32 ? 5 : (w == 16 ? 4 : 3);
+}
+
+// kernel S count-store policy (escape_kernels.cuh, "Output sectors"): FRACTAL_STAGE=
+// 3 L2 evict_last stores (default), 1|2 shared-memory staging, 0 plain stores
+int stage_counts() {
+  static const int v = env_int("FRACTAL_STAGE", 3);
+  return v;
+}
+
 // Parameter derivation in binary64: hx = half_w / W, hy = half_h / H.
 fr::Geom make_geom(fr_window win, int32_t width, int32_t height, int32_t max_iter,
                    fr_bands b, int64_t rows, uint16_t* counts, uint8_t* rgba) {
@@ -106,6 +119,8 @@ fr::Geom make_geom(fr_window win, int32_t width, int32_t height, int32_t max_ite
   g.counts = counts;
   g.counts8 = nullptr;
   g.rgba = reinterpret_cast<uchar4*>(rgba);
+  g.wlog = warp_tile_log();
+  g.stage = stage_counts();
   return g;
 }
 
