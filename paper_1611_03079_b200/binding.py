@@ -87,10 +87,17 @@ def load():
     with _lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(LIB_PATH):
-            raise FractalError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; "
+        path = LIB_PATH
+        alt = os.environ.get("FRACTAL_LIB")  # diagnostic: a build.build_variant library
+        if alt:
+            alt = os.path.realpath(alt)
+            if os.path.dirname(alt) != os.path.join(os.path.dirname(LIB_PATH), "variants"):
+                raise FractalError(f"FRACTAL_LIB must name a library under variants/: {alt}")
+            path = alt
+        if not os.path.exists(path):
+            raise FractalError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; "
                                "g.build()'` (there is no CPU fallback)")
-        lib = ctypes.CDLL(LIB_PATH)
+        lib = ctypes.CDLL(path)
         st, vp, i32, i64 = ctypes.c_int, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
         P = ctypes.POINTER
         lib.julia_render.argtypes = [_Complex, _Window, i32, i32, i32, vp, vp]

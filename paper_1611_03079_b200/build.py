@@ -36,5 +36,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Diagnostic build of libfractal with extra -D flags into variants/ (same-box A/B
+    of compile-time choices; loaded through FRACTAL_LIB, see binding.load)."""
+    out_dir = os.path.join(PKG, "variants")
+    os.makedirs(out_dir, exist_ok=True)
+    out = os.path.join(out_dir, f"libfractal_{name}.so")
+    subprocess.check_call([NVCC, *FLAGS, *[f"-D{d}" for d in defines], *SOURCES, "-o", out])
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

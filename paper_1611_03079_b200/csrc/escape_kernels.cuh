@@ -39,8 +39,6 @@ struct Geom {
   uint16_t* counts;
   uint8_t* counts8;  // uint8 counts instead (max_iter <= 255; static kernel only), else null
   uchar4* rgba;   // nullptr unless colour levels are fused
-  int stage;      // kernel S path chunks: stage counts in shared memory (whole-sector writes)
-  int wlog;       // kernel S warp tile (1 << wlog) x (32 >> wlog): 3 -> 8x4, 4 -> 16x2, 5 -> 32x1
 };
 
 // Julia C values of a path chunk, already in the kernel's state representation
@@ -458,11 +456,13 @@ constexpr bool kAsmLoop = std::is_same<T, float>::value && !STRICT && (K == 2 ||
 // count is exact per iteration (sticky alive predicate + predicated increment).
 // MANDEL takes C from the pixel and Z_0 = 0.
 // ----------------------------------------------------------------------------------
-template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int NC, int FN = 0>
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int NC, int FN = 0, int ES = 2>
 __global__ void __launch_bounds__(kThreads)
 escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int frame0,
                    int n_frames, int fpc) {
   static_assert(FN == 0 || (STRICT && !MANDEL), "map variants: strict Julia frames");
+  static_assert(ES == 1 || ES == 2, "counts are uint16 (ES 2) or uint8 (ES 1)");
+  using CountT = typename std::conditional<ES == 2, uint16_t, uint8_t>::type;
   __shared__ uchar4 spal[COLOR ? 256 : 1];
   const int tile = blockIdx.x;
   const int ty = tile / g.tiles_x;
@@ -473,13 +473,8 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
   }
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  // 8x4 warp tiles (orbit coherence), or 16x2 / 32x1 so each warp row writes whole
-  // 32-B sectors of uint16 / uint8 counts: with frame groups the warps of a CTA drift apart in
-  // frames, and a sector half-written by two warps can leave L2 in between (DRAM
-  // read-modify-write)
-  const int wl = g.wlog, hl = 5 - wl;  // warp tile (1 << wl) x (1 << hl)
-  const int cx = ((warp & ((1 << hl) - 1)) << wl) + (lane & ((1 << wl) - 1));
-  const int cy = ((warp >> hl) << hl) + (lane >> wl);
+  const int cx = (warp & 3) * kWarpW + (lane & 7);
+  const int cy = (warp >> 2) * kWarpH + (lane >> 3);
   const int px = tx * kTileW + cx;
   const int ly = ty * kTileH + cy;
   const bool inside = (px < g.W) && (ly < g.rows);
@@ -493,40 +488,39 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
   const int f1 = min(f0 + fpc, n_frames);
   const int64_t stride = g.frame_stride;
   const int64_t pix0 = (int64_t)(frame0 + f0) * stride + (int64_t)ly * g.W + px;
-  // counts are uint16, or uint8 when g.counts8 is set (max_iter <= 255): byte addressing
-  const int es = g.counts8 ? 1 : 2;
-  char* outp = g.counts8 ? reinterpret_cast<char*>(g.counts8 + pix0)
-                         : reinterpret_cast<char*>(g.counts + pix0);
-  const int64_t bstride = stride * es;
+  CountT* outp = (ES == 2 ? reinterpret_cast<CountT*>(g.counts)
+                          : reinterpret_cast<CountT*>(g.counts8)) + pix0;
   uchar4* outc = COLOR ? g.rgba + pix0 : nullptr;
   // Output sectors: with 8x4 warp tiles each 32-B sector of a count row is written half
   // by one warp and half by its neighbour, and over a frame group the two warps drift
   // apart in frames; a sector evicted from L2 half-written costs a DRAM read-modify-write
-  // (measured: +0.4 GB reads per cfg4 launch).  g.stage selects the remedy:
-  //   3 (default): direct stores with an L2 evict_last policy, so the half-written line
-  //      stays in L2 until its other half arrives (no extra instructions);
-  //   1 / 2: path chunks stage the group's counts in shared memory and write whole 16-B
-  //      row segments after a warp-pair named barrier (1) or a CTA barrier (2);
-  //   0: plain direct stores.
+  // (measured: +0.4 GB reads per cfg4 launch).  FR_COUNT_STORE (compile time) picks the
+  // count store: 1 (default) L2 evict_last policy, so a half-written line tends to stay
+  // until its other half arrives; 2 stage the frame group in shared memory and write
+  // whole 16-B row segments after a CTA barrier (path chunks); 0 plain stores.
+  // DESIGN.md §5 has the measurements.
+#ifndef FR_COUNT_STORE
+#define FR_COUNT_STORE 1
+#endif
+  constexpr bool kStaged = FR_COUNT_STORE == 2 && NC > 1;
   constexpr int kStageFrames = 32;
-  __shared__ __align__(16) uint16_t stage[NC > 1 ? kStageFrames * kThreads : 1];
-  const bool staged = NC > 1 && (g.stage == 1 || g.stage == 2) && (f1 - f0) <= kStageFrames;
-  uint16_t* sp = stage + cy * kTileW + cx;
+  __shared__ __align__(16) CountT stage[kStaged ? kStageFrames * kThreads : 1];
+  const bool staged = kStaged && (f1 - f0) <= kStageFrames;
+  CountT* sp = stage + cy * kTileW + cx;
   uint64_t l2pol = 0;
-  if (g.stage == 3) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(l2pol));
-  auto put = [&](char* q, int v) {
-    if (staged) {
-      *sp = (uint16_t)v;
-    } else if (g.stage == 3 && es == 2) {
-      asm volatile("st.global.L2::cache_hint.u16 [%0], %1, %2;" ::"l"(q), "h"((unsigned short)v),
-                   "l"(l2pol) : "memory");
-    } else if (g.stage == 3) {
+  if (FR_COUNT_STORE == 1)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(l2pol));
+  auto put = [&](CountT* q, int v, int dk) {  // dk: frame offset of q from outp (0 or 1)
+    if (kStaged && staged) {
+      sp[dk * kThreads] = (CountT)v;
+    } else if constexpr (FR_COUNT_STORE == 1 && ES == 2) {
+      asm volatile("st.global.L2::cache_hint.u16 [%0], %1, %2;" ::"l"(q),
+                   "h"((unsigned short)v), "l"(l2pol) : "memory");
+    } else if constexpr (FR_COUNT_STORE == 1) {
       asm volatile("st.global.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(q), "r"(v), "l"(l2pol)
                    : "memory");
-    } else if (es == 2) {
-      *reinterpret_cast<uint16_t*>(q) = (uint16_t)v;
     } else {
-      *reinterpret_cast<uint8_t*>(q) = (uint8_t)v;
+      *q = (CountT)v;
     }
   };
 
@@ -537,8 +531,14 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
       float x = are, y = aim, x2 = are, y2 = aim;
       unsigned alive = inside ? 1u : 0u, alive2 = alive;
       int cnt = 0, cnt2 = 0;
-      int n = fast_vote_loop2_f32<K>(x, y, cnt, alive, x2, y2, cnt2, alive2, cs.re[f], cs.im[f],
-                                     cs.re[f + 1], cs.im[f + 1], kfull);
+      // C values through a shuffle: they then live in per-thread registers, so the FFMA
+      // X' = T * 0.5 + CR2 keeps 0.5 as an immediate (a uniform-register C forces ptxas
+      // to rematerialise 0.5 with an extra ALU move every iteration: +18% instructions)
+      int n = fast_vote_loop2_f32<K>(x, y, cnt, alive, x2, y2, cnt2, alive2,
+                                     __shfl_sync(kFull, cs.re[f], lane),
+                                     __shfl_sync(kFull, cs.im[f], lane),
+                                     __shfl_sync(kFull, cs.re[f + 1], lane),
+                                     __shfl_sync(kFull, cs.im[f + 1], lane), kfull);
       if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
         for (; n < max_iter; ++n) {
           Iter<T, STRICT>::step(x, y, cs.re[f], cs.im[f], alive, cnt);
@@ -547,17 +547,15 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
       }
       if (inside) {
         const int c1 = min(cnt, max_iter), c2 = min(cnt2, max_iter);
-        put(outp, c1);
-        sp += kThreads;
-        put(outp + bstride, c2);
-        sp -= kThreads;
+        put(outp, c1, 0);
+        put(outp + stride, c2, 1);
         if (COLOR) {
           outc[0] = colour_of(spal, pal, c1, max_iter);
           outc[stride] = colour_of(spal, pal, c2, max_iter);
         }
       }
-      outp += 2 * bstride;
-      sp += 2 * kThreads;
+      outp += 2 * stride;
+      if (kStaged) sp += 2 * kThreads;
       if (COLOR) outc += 2 * stride;
     }
   }
@@ -594,58 +592,34 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
     }
     if (inside) {
       const int count = min(cnt, max_iter);
-      put(outp, count);
+      put(outp, count, 0);
       if (COLOR) *outc = colour_of(spal, pal, count, max_iter);
     }
-    outp += bstride;
-    sp += kThreads;
+    outp += stride;
+    if (kStaged) sp += kThreads;
     if (COLOR) outc += stride;
   }
-  if (NC > 1 && staged) {
-    // flush: only the two warps of a pair share output sectors, so each pair syncs on its
-    // own named barrier and writes its 16x4 region (8x4 warp tiles; other warp tiles use
-    // the CTA barrier).  Each thread owns one segment (row, 8-pixel group) and walks the
-    // frames 8 apart: a 16-B (uint16) or 8-B (uint8) vector store when the segment is
-    // whole and aligned in every frame, else per pixel within bounds.
-    int t, r, col;
-    if (g.wlog == 3 && g.stage == 1) {
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + (warp >> 1)) : "memory");
-      t = threadIdx.x & 63;
-      r = (warp >> 2) * 4 + ((t >> 1) & 3);
-      col = ((warp >> 1) & 1) * 16 + (t & 1) * 8;
-    } else {
+  if constexpr (kStaged) {
+    if (staged) {
+      // flush: thread = (row, 8-pixel group) segment, frames 8 apart; vector store when
+      // the segment is whole and aligned in every frame, else per pixel in bounds
       __syncthreads();
-      t = threadIdx.x;
-      r = (t >> 2) & 7;
-      col = (t & 3) * 8;
-    }
-    const int fl0 = t >> (g.wlog == 3 && g.stage == 1 ? 3 : 5);  // 0..7
-    const int row = ty * kTileH + r;
-    const int x0 = tx * kTileW + col;
-    if (row < g.rows && x0 < g.W) {
-      const int64_t e = (int64_t)(frame0 + f0 + fl0) * stride + (int64_t)row * g.W + x0;
-      char* q = g.counts8 ? reinterpret_cast<char*>(g.counts8 + e)
-                          : reinterpret_cast<char*>(g.counts + e);
-      const uint16_t* src = stage + fl0 * kThreads + r * kTileW + col;
-      const int64_t qstep = 8 * bstride;
-      const int nf = f1 - f0;
-      const unsigned amask = es == 2 ? 15u : 7u;
-      const bool vec = x0 + 8 <= g.W && (reinterpret_cast<uintptr_t>(q) & amask) == 0 &&
-                       (bstride & amask) == 0;
-      for (int fl = fl0; fl < nf; fl += 8, q += qstep, src += 8 * kThreads) {
-        const uint4 v = *reinterpret_cast<const uint4*>(src);
-        if (vec && es == 2) {
-          *reinterpret_cast<uint4*>(q) = v;
-        } else if (vec) {
-          // counts <= 255 here: keep the low byte of each uint16
-          *reinterpret_cast<uint2*>(q) =
-              make_uint2(__byte_perm(v.x, v.y, 0x6420), __byte_perm(v.z, v.w, 0x6420));
-        } else {
-          const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
-          const int n = min(8, g.W - x0);
-          for (int i = 0; i < n; ++i) {
-            if (es == 2) reinterpret_cast<uint16_t*>(q)[i] = h[i];
-            else reinterpret_cast<uint8_t*>(q)[i] = (uint8_t)h[i];
+      const int t = threadIdx.x, r = (t >> 2) & 7, col = (t & 3) * 8, fl0 = t >> 5;
+      const int row = ty * kTileH + r, x0 = tx * kTileW + col;
+      if (row < g.rows && x0 < g.W) {
+        CountT* q = (ES == 2 ? reinterpret_cast<CountT*>(g.counts)
+                             : reinterpret_cast<CountT*>(g.counts8)) +
+                    ((int64_t)(frame0 + f0 + fl0) * stride + (int64_t)row * g.W + x0);
+        const CountT* src = stage + fl0 * kThreads + r * kTileW + col;
+        constexpr unsigned kVec = 8 * ES;  // bytes per segment
+        const bool vec = x0 + 8 <= g.W && (reinterpret_cast<uintptr_t>(q) % kVec) == 0 &&
+                         ((stride * ES) % kVec) == 0;
+        for (int fl = fl0; fl < f1 - f0; fl += 8, q += 8 * stride, src += 8 * kThreads) {
+          if (vec) {
+            if constexpr (ES == 2) *reinterpret_cast<uint4*>(q) = *reinterpret_cast<const uint4*>(src);
+            else *reinterpret_cast<uint2*>(q) = *reinterpret_cast<const uint2*>(src);
+          } else {
+            for (int i = 0; i < min(8, g.W - x0); ++i) q[i] = src[i];
           }
         }
       }

@@ -86,19 +86,6 @@ fr_status make_palette(const fr_palette* pal, fr::Palette* out) {
   return FR_OK;
 }
 
-// kernel S warp tile width 8|16|32 (FRACTAL_WTILE), as log2
-int warp_tile_log() {
-  static const int w = env_int("FRACTAL_WTILE", 8);
-  return w == 32 ? 5 : (w == 16 ? 4 : 3);
-}
-
-// kernel S count-store policy (escape_kernels.cuh, "Output sectors"): FRACTAL_STAGE=
-// 3 L2 evict_last stores (default), 1|2 shared-memory staging, 0 plain stores
-int stage_counts() {
-  static const int v = env_int("FRACTAL_STAGE", 3);
-  return v;
-}
-
 // Parameter derivation in binary64: hx = half_w / W, hy = half_h / H.
 fr::Geom make_geom(fr_window win, int32_t width, int32_t height, int32_t max_iter,
                    fr_bands b, int64_t rows, uint16_t* counts, uint8_t* rgba) {
@@ -119,8 +106,6 @@ fr::Geom make_geom(fr_window win, int32_t width, int32_t height, int32_t max_ite
   g.counts = counts;
   g.counts8 = nullptr;
   g.rgba = reinterpret_cast<uchar4*>(rgba);
-  g.wlog = warp_tile_log();
-  g.stage = stage_counts();
   return g;
 }
 
@@ -151,12 +136,20 @@ cudaError_t launch_tiles_t(const fr::Geom& g, const fr::Palette& pal, const fr::
       return cudaGetLastError();
     }
   }
-  if (sizeof(T) == 4 && !STRICT && static_k() == 2)
+  constexpr int KD = sizeof(T) == 8 ? 2 * kStaticK : kStaticK;
+  if (g.counts8 != nullptr) {  // uint8 counts: path chunks only (julia_render_path8)
+    if constexpr (NC > 1 && !MANDEL)
+      fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, KD, NC, 0, 1>
+          <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);
+    else
+      return cudaErrorInvalidValue;
+  } else if (sizeof(T) == 4 && !STRICT && static_k() == 2) {
     fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, 2, NC>
         <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);
-  else
-    fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, (sizeof(T) == 8 ? 2 * kStaticK : kStaticK), NC>
+  } else {
+    fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, KD, NC>
         <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

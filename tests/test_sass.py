@@ -1,0 +1,67 @@
+"""Static checks on the built sm_100a code (cuobjdump, no GPU): the escape kernels are
+compiled for sm_100a, do not spill to local memory, and the fast fp32 loops keep the
+constant 0.5 of X' = T * 0.5 + CR2 as an FFMA immediate.  ptxas rematerialises 0.5
+with an extra ALU move every iteration when C sits in a uniform register (DESIGN.md
+§5, "SASS guard"); that cost +18% instructions on the bench kernel before it was
+caught, so it is pinned here."""
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from paper_1611_03079_b200 import build
+
+pytestmark = pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="no cuobjdump")
+
+
+@pytest.fixture(scope="module")
+def sass():
+    build.build()
+    out = subprocess.run(["cuobjdump", "-sass", build.LIB], capture_output=True, text=True,
+                         check=True).stdout
+    funcs, name = {}, None
+    for line in out.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            name = m.group(1)
+            funcs[name] = []
+            continue
+        if name is not None:
+            ins = re.sub(r"/\*\s*0x[0-9a-f]+\s*\*/", "", line)  # drop encoding words
+            ins = re.sub(r"^\s*/\*[0-9a-f]+\*/", "", ins).strip()
+            if ins:
+                funcs[name].append(ins)
+    return out, funcs
+
+
+def _fast_f32(name):
+    # escape_tile_kernel / escape_refill_kernel with T = float, STRICT = false; tile2
+    return (re.search(r"escape_(tile|refill)_kernelIfLb0E", name) is not None
+            or "escape_tile2_kernel" in name)
+
+
+def test_sm100a(sass):
+    out, funcs = sass
+    assert "arch = sm_100a" in out
+    assert any("escape_tile_kernel" in f for f in funcs)
+    assert any("colorize_kernel" in f for f in funcs)
+
+
+def test_no_local_memory_spills(sass):
+    _, funcs = sass
+    for name, ins in funcs.items():
+        if "escape" in name or "colorize" in name:
+            bad = [i for i in ins if re.search(r"\b(LDL|STL)\b", i)]
+            assert not bad, (name, bad[:3])
+
+
+def test_half_stays_an_immediate(sass):
+    _, funcs = sass
+    fast = [n for n in funcs if _fast_f32(n)]
+    assert len(fast) >= 10
+    for name in fast:
+        remat = [i for i in funcs[name] if re.search(r"MOV.*0x3f000000", i)]
+        assert not remat, (name, remat[:3])
+        assert any(re.search(r"FFMA .*, 0\.5, ", i) for i in funcs[name]), name
