@@ -303,14 +303,19 @@ def main():
             "clocks": clocks,
             "roofline": roof,
         }
-    # ---- the exchange step (N > 1): NCCL gather of every rank's frames to rank 0
+    # ---- the exchange step (N > 1): NCCL gather of every rank's frames to rank 0, plain
+    # (after the render) and pipelined with the render (chunked, separate stream)
     gather = measure_gather(out, world, rank, barrier) if world > 1 else None
+    delivered = (measure_delivered(win, world, rank, barrier, job_iters / args.steps)
+                 if world > 1 else None)
     # ---- end-to-end through the public API with HOST buffers (pinned), N GPUs
     e2e = measure_e2e(fr, W, cs, win, world, args, barrier, stream)
     if rank == 0:
         line["e2e"] = e2e
         if gather is not None:
             line["gather_to_rank0"] = gather
+        if delivered is not None:
+            line["delivered_to_rank0"] = delivered
         if world == 1:
             line["cpu_baseline"] = cpu_oracle_rate(cs, seconds=args.cpu_seconds)
             if not args.no_extra:
@@ -349,6 +354,41 @@ def measure_gather(out, world, rank, barrier):
         return {"ms": ms, "bytes_into_rank0": nbytes, "GB_per_s": nbytes / (ms * 1e-3) / 1e9,
                 "note": "uint16 frames of ranks 1..N-1 to rank 0 (NCCL gather, uint8 view); "
                         "the rank-0 ingress bound is ~0.77-0.9 TB/s (B200_PROFILING.md)"}
+    except Exception as e:  # report, never fail the bench line
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+
+
+def measure_delivered(win, world, rank, barrier, job_iters_per_step, chunk=64):
+    """Frames delivered to rank 0 with the render and the gather pipelined
+    (distributed.deliver_path: chunks of `chunk` frames per rank, uint8 counts, gather on
+    its own stream overlapping the next chunk's render), max over ranks -- the second
+    frames/s figure of SURVEY §8(e) next to the compute-resident `value`."""
+    import torch
+    import torch.distributed as dist
+    from paper_1611_03079_b200 import distributed as D
+    from paper_1611_03079_b200 import workloads as W
+    try:
+        full = W.circle_path(FRAMES_PER_RANK * world, RADIUS)
+        got = D.deliver_path(full, win, W_PX, H_PX, MAX_ITER, chunk=chunk)  # warm-up
+        del got
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        got = D.deliver_path(full, win, W_PX, H_PX, MAX_ITER, chunk=chunk)
+        t1.record()
+        barrier()
+        del got
+        t = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        nbytes = FRAMES_PER_RANK * W_PX * H_PX * (world - 1)
+        return {"ms": ms, "frames_per_s": len(full) / (ms * 1e-3),
+                "gpix_iter_s": job_iters_per_step / (ms * 1e-3) / 1e9,
+                "bytes_into_rank0": nbytes, "ingress_GB_per_s": nbytes / (ms * 1e-3) / 1e9,
+                "chunk_frames_per_rank": chunk, "dtype": "u8",
+                "note": "render + NCCL gather to rank 0 pipelined per chunk (separate stream); "
+                        "frames land in rank 0's buffer, path order is a zero-copy view"}
     except Exception as e:  # report, never fail the bench line
         return {"error": f"{type(e).__name__}: {e}"[:300]}
 

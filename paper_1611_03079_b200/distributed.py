@@ -16,6 +16,7 @@ rank contributes the same padded size.
 """
 from __future__ import annotations
 
+import contextlib
 import math
 
 import numpy as np
@@ -112,6 +113,93 @@ def gather_bands(local: torch.Tensor, height: int, band_rows: int, dst: int = 0,
     world = dist.get_world_size(group)
     parts = gather_padded(local, max_band_rows(height, band_rows, world), dst, group)
     return assemble_bands(parts, height, band_rows) if parts is not None else None
+
+
+# --------------------------------------------------------------------------- pipelined delivery
+class Delivered:
+    """Frames delivered to rank dst by `deliver_path`: the receive buffer
+    [n_chunks, world, chunk, H, W] as NCCL filled it.  Frame k (path order) is
+    buf[j, r, i] with r = k % world and k // world = j * chunk + i, so path order is the
+    zero-copy view buf.permute(0, 2, 1, 3, 4) ("rank 0 un-interleaves with
+    a view or one HBM-bound copy")."""
+
+    def __init__(self, buf: torch.Tensor, n_frames: int, world: int, chunk: int):
+        self.buf, self.n_frames, self.world, self.chunk = buf, n_frames, world, chunk
+
+    def frame(self, k: int) -> torch.Tensor:
+        idx, r = divmod(k, self.world)
+        j, i = divmod(idx, self.chunk)
+        return self.buf[j, r, i]
+
+    def path_view(self) -> torch.Tensor:
+        """[n_chunks, chunk, world, H, W] view whose flattening is path order (padded)."""
+        return self.buf.permute(0, 2, 1, 3, 4)
+
+    def to_path_order(self) -> torch.Tensor:
+        """The frames in path order as one contiguous tensor (one HBM-bound copy)."""
+        v = self.path_view()
+        return v.reshape((-1,) + tuple(v.shape[3:]))[: self.n_frames]
+
+
+def deliver_path(cs, win, width: int, height: int, max_iter: int = 100, mode=None,
+                 chunk: int = 64, dst: int = 0, group=None, dtype=torch.uint8, render=None,
+                 device=None):
+    """Render this rank's cyclic frames of the path in chunks of `chunk` frames and
+    gather every chunk to `dst` while the next chunk renders (SURVEY §8(e) plan 1):
+    render on the current stream into one of two buffers, gather on a separate
+    communication stream; a buffer is rendered again only after its previous gather
+    finished (CUDA events).  uint8 counts (max_iter <= 255) halve the bytes on the wire.
+
+    `render(cs_chunk, out)` fills out[:len(cs_chunk)] (default: libfractal's
+    julia_render_path on `out`'s device); the CPU tests pass a synthetic one under gloo.
+    Returns a `Delivered` on dst, None elsewhere."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    cs = np.asarray(cs, dtype=np.complex128).reshape(-1)
+    n = len(cs)
+    if dtype == torch.uint8 and max_iter > 255:
+        raise ValueError("uint8 delivery needs max_iter <= 255")
+    if render is None:
+        from . import binding as fr
+        md = fr.Mode.FP32_FAST if mode is None else mode
+
+        def render(c, out):
+            fr.julia_render_path(c, win, width, height, max_iter, md, out=out)
+        device = torch.device("cuda", torch.cuda.current_device())
+    device = torch.device("cpu") if device is None else torch.device(device)
+    k_local = frame_indices(n, world, rank)
+    n_chunks = max(1, math.ceil(frames_per_rank(n, world) / chunk))
+    bufs = [torch.zeros((chunk, height, width), dtype=dtype, device=device) for _ in range(2)]
+    recv = (torch.empty((n_chunks, world, chunk, height, width), dtype=dtype, device=device)
+            if rank == dst else None)
+    cuda = device.type == "cuda"
+    comp = torch.cuda.current_stream(device) if cuda else None
+    comm = torch.cuda.Stream(device) if cuda else None
+    done = [None, None]
+    for j in range(n_chunks):
+        b = j % 2
+        lo, hi = j * chunk, min((j + 1) * chunk, len(k_local))
+        if cuda and done[b] is not None:
+            comp.wait_event(done[b])
+        if hi > lo:
+            render(cs[k_local[lo:hi]], bufs[b][: hi - lo])
+        if cuda:
+            ready = torch.cuda.Event()
+            ready.record(comp)
+            comm.wait_event(ready)
+        with torch.cuda.stream(comm) if cuda else contextlib.nullcontext():
+            send = bufs[b].reshape(-1).view(torch.uint8)
+            if rank == dst:
+                gl = [recv[j, r].reshape(-1).view(torch.uint8) for r in range(world)]
+                dist.gather(send, gather_list=gl, dst=dst, group=group)
+            else:
+                dist.gather(send, dst=dst, group=group)
+            if cuda:
+                done[b] = torch.cuda.Event()
+                done[b].record(comm)
+    if cuda:
+        comp.wait_stream(comm)
+    return Delivered(recv, n, world, chunk) if rank == dst else None
 
 
 # --------------------------------------------------------------------------- GPU renders

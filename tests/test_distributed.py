@@ -100,3 +100,45 @@ def test_gather_frames_and_bands_gloo(world):
         assert p.exitcode == 0
     ok_f, ok_b = q.get(timeout=10)
     assert ok_f and ok_b
+
+
+def _deliver_worker(rank, world, port, q, n, chunk, dtype):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cs = np.arange(n, dtype=np.float64) + 0j  # C_k = k tags the frame
+
+        def render(c, out):  # frame k -> every pixel (7k + 1) mod 251, rank-local shape
+            v = torch.as_tensor((7 * np.real(c).astype(np.int64) + 1) % 251, dtype=out.dtype)
+            out[: len(c)] = v[:, None, None]
+
+        got = D.deliver_path(cs, None, 5, 3, 100, chunk=chunk, render=render, dtype=dtype)
+        if rank == 0:
+            want = torch.stack([torch.full((3, 5), (7 * k + 1) % 251, dtype=dtype) for k in range(n)])
+            ok = torch.equal(got.to_path_order(), want) and all(
+                torch.equal(got.frame(k), want[k]) for k in range(n))
+            q.put(ok)
+        else:
+            assert got is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,chunk,dtype", [(2, 13, 2, torch.uint8), (3, 13, 4, torch.int16),
+                                                 (2, 3, 8, torch.uint8), (3, 2, 1, torch.uint8)])
+def test_deliver_path_pipelined_gloo(world, n, chunk, dtype):
+    """Chunked render + gather to rank 0 (SURVEY §8(e) plan 1): every frame arrives, in
+    path order through the zero-copy view, including ranks with no frames and ragged
+    last chunks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_deliver_worker, args=(r, world, port, q, n, chunk, dtype))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert q.get(timeout=10)

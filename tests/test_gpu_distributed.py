@@ -62,3 +62,22 @@ def test_render_bands_nccl(nccl, kind):
         ref = fr.mandelbrot_param_map(win, w, h, 300, fr.Mode.FP64_FAST)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(_np16(img), _np16(ref))
+
+
+@pytest.mark.parametrize("chunk", [1, 5, 64])
+def test_deliver_path_nccl(nccl, chunk):
+    """Pipelined render + gather (distributed.deliver_path) on the real renderer: the
+    delivered frames equal one julia_render_path call (uint8 counts), ragged last chunk
+    included."""
+    from paper_1611_03079_b200 import binding as fr
+    from paper_1611_03079_b200 import distributed as D
+    from paper_1611_03079_b200 import workloads as W
+    cs = W.circle_path(23)
+    win = W.julia_window(320, 180)
+    got = D.deliver_path(cs, win, 320, 180, 100, fr.Mode.FP32_STRICT, chunk=chunk)
+    ref = fr.julia_render_path(cs, win, 320, 180, 100, fr.Mode.FP32_STRICT,
+                               out=torch.empty((23, 180, 320), dtype=torch.uint8, device="cuda"))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.to_path_order().cpu().numpy(), ref.cpu().numpy())
+    for k in (0, 11, 22):
+        np.testing.assert_array_equal(got.frame(k).cpu().numpy(), ref[k].cpu().numpy())
