@@ -130,10 +130,28 @@ def cpu_oracle_rate(cs, seconds: float = 12.0, threads: int | None = None):
         if time.perf_counter() - t0 >= seconds:
             break
     dt = time.perf_counter() - t0
-    return {"value": total / dt / 1e9, "unit": "Gpixel-iter/s", "cores": threads,
-            "kind": "oracle", "frames_per_s": frames / dt,
-            "sample": f"{frames} of the {len(cs)} rank-0 1080p frames (random order), strict "
-                      f"fp32 scalar C oracle, {threads} threads, {dt:.1f} s"}
+    res = {"value": total / dt / 1e9, "unit": "Gpixel-iter/s", "cores": threads,
+           "kind": "oracle", "frames_per_s": frames / dt,
+           "sample": f"{frames} of the {len(cs)} rank-0 1080p frames (random order), strict "
+                     f"fp32 scalar C oracle, {threads} threads, {dt:.1f} s"}
+    if threads > 1:
+        # also once on one core (same frames, ~1/4 of the time budget)
+        t1, tot1, fr1 = time.perf_counter(), 0, 0
+        for k in order:
+            g = oracle.julia(complex(cs[k]), win.center, win.half_w, win.half_h, W_PX, H_PX,
+                             MAX_ITER, 32, 1)
+            tot1 += int(g.sum(dtype=np.int64))
+            fr1 += 1
+            if time.perf_counter() - t1 >= seconds / 4:
+                break
+        d1 = time.perf_counter() - t1
+        res["one_core"] = {"value": tot1 / d1 / 1e9, "frames": fr1, "seconds": round(d1, 2)}
+    try:
+        res["cpu_model"] = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo")
+                                if l.startswith("model name"))
+    except Exception:
+        pass
+    return res
 
 
 def run_reference(args, rank, world):
