@@ -39,7 +39,23 @@ struct Geom {
   uint16_t* counts;
   uint8_t* counts8;  // uint8 counts instead (max_iter <= 255; static kernel only), else null
   uchar4* rgba;   // nullptr unless colour levels are fused
+  int grid2d;     // kernels S/S2: tiles on grid x/y (frame groups on z), else tiles on x
 };
+
+// Tile (and frame group) of this CTA for kernels S/S2.  With grid2d the launch is
+// (tiles_x, tiles_y, groups) and no division is needed; otherwise (tiles_y > 65535)
+// tiles are linear on x and groups on y.
+__device__ __forceinline__ void tile_of(const Geom& g, int& tx, int& ty, int& grp) {
+  if (g.grid2d) {
+    tx = blockIdx.x;
+    ty = blockIdx.y;
+    grp = blockIdx.z;
+  } else {
+    ty = blockIdx.x / g.tiles_x;
+    tx = blockIdx.x - ty * g.tiles_x;
+    grp = blockIdx.y;
+  }
+}
 
 // Julia C values of a path chunk, already in the kernel's state representation
 // (rounded once to T on the host; doubled in FAST modes -- exact), so the kernel does no
@@ -464,9 +480,8 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
   static_assert(ES == 1 || ES == 2, "counts are uint16 (ES 2) or uint8 (ES 1)");
   using CountT = typename std::conditional<ES == 2, uint16_t, uint8_t>::type;
   __shared__ uchar4 spal[COLOR ? 256 : 1];
-  const int tile = blockIdx.x;
-  const int ty = tile / g.tiles_x;
-  const int tx = tile - ty * g.tiles_x;
+  int tx, ty, grp;
+  tile_of(g, tx, ty, grp);
   if (COLOR) {
     spal[threadIdx.x] = pal.e[threadIdx.x];
     __syncthreads();
@@ -484,7 +499,7 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
   const T aim = to_state<T, STRICT>(pixel_im(g, global_row(g, min(ly, g.rows - 1))));
   const int max_iter = g.max_iter;
   const int kfull = max_iter - max_iter % K;  // iterations run in whole K-blocks
-  const int f0 = blockIdx.y * fpc;
+  const int f0 = grp * fpc;
   const int f1 = min(f0 + fpc, n_frames);
   const int64_t stride = g.frame_stride;
   const int64_t pix0 = (int64_t)(frame0 + f0) * stride + (int64_t)ly * g.W + px;
@@ -546,7 +561,9 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
         }
       }
       if (inside) {
-        const int c1 = min(cnt, max_iter), c2 = min(cnt2, max_iter);
+        // counts need no clamp: one increment at most per executed iteration, and the
+        // loops execute exactly max_iter iterations at most
+        const int c1 = cnt, c2 = cnt2;
         put(outp, c1, 0);
         put(outp + stride, c2, 1);
         if (COLOR) {
@@ -591,7 +608,7 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
       for (; n < max_iter; ++n) It::step(x, y, cr, ci, alive, cnt);
     }
     if (inside) {
-      const int count = min(cnt, max_iter);
+      const int count = cnt;  // <= max_iter (see above)
       put(outp, count, 0);
       if (COLOR) *outc = colour_of(spal, pal, count, max_iter);
     }
@@ -638,9 +655,8 @@ template <bool MANDEL, bool COLOR>
 __global__ void __launch_bounds__(kThreads)
 escape_tile2_kernel(const Geom g, const Palette pal, const float jcr2, const float jci2) {
   __shared__ uchar4 spal[COLOR ? 256 : 1];
-  const int tile = blockIdx.x;
-  const int ty = tile / g.tiles_x;
-  const int tx = tile - ty * g.tiles_x;
+  int tx, ty, grp;
+  tile_of(g, tx, ty, grp);
   if (COLOR) {
     spal[threadIdx.x] = pal.e[threadIdx.x];
     __syncthreads();
@@ -685,13 +701,13 @@ escape_tile2_kernel(const Geom g, const Palette pal, const float jcr2, const flo
   }
   if (in0) {
     const int64_t off = (int64_t)ly0 * g.W + px;
-    const int c0 = min(cnt, max_iter);
+    const int c0 = cnt;  // <= max_iter: at most one increment per executed iteration
     g.counts[off] = (uint16_t)c0;
     if (COLOR) g.rgba[off] = colour_of(spal, pal, c0, max_iter);
   }
   if (in1) {
     const int64_t off = (int64_t)ly1 * g.W + px;
-    const int c1 = min(cnt2, max_iter);
+    const int c1 = cnt2;
     g.counts[off] = (uint16_t)c1;
     if (COLOR) g.rgba[off] = colour_of(spal, pal, c1, max_iter);
   }

@@ -106,6 +106,7 @@ fr::Geom make_geom(fr_window win, int32_t width, int32_t height, int32_t max_ite
   g.counts = counts;
   g.counts8 = nullptr;
   g.rgba = reinterpret_cast<uchar4*>(rgba);
+  g.grid2d = 0;
   return g;
 }
 
@@ -117,25 +118,33 @@ int static_k() {
 }
 constexpr int kFramesPerCta = 32;  // frames of a path chunk rendered per CTA (static kernel); FRACTAL_FPC overrides
 
+// Launch grid of kernels S/S2: (tiles_x, tiles_y, groups) when tiles_y fits grid y
+// (kernel-side tile_of needs no division), else (tiles_x * tiles_y, groups, 1).
+dim3 tile_grid(fr::Geom& g, int64_t tiles_y, int groups) {
+  g.grid2d = tiles_y <= 65535 ? 1 : 0;
+  if (g.grid2d) return dim3((unsigned)g.tiles_x, (unsigned)tiles_y, (unsigned)groups);
+  return dim3((unsigned)((int64_t)g.tiles_x * tiles_y), (unsigned)groups, 1);
+}
+
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int NC>
-cudaError_t launch_tiles_t(const fr::Geom& g, const fr::Palette& pal, const fr::CList<T, NC>& cs,
+cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr::CList<T, NC>& cs,
                            int n_frames, int frame0, cudaStream_t s) {
-  const int64_t tiles = (int64_t)g.tiles_x * ((g.rows + fr::kTileH - 1) / fr::kTileH);
+  fr::Geom g = g0;
   static const int fpc_env = env_int("FRACTAL_FPC", 0);
   const int fpc_want = fpc_env > 0 ? fpc_env : kFramesPerCta;
   const int fpc = n_frames < fpc_want ? n_frames : fpc_want;
-  dim3 grid((unsigned)tiles, (unsigned)((n_frames + fpc - 1) / fpc), 1);
   // one frame, fast fp32: two pixels per thread (kernel S2; FRACTAL_S2=0 disables)
   static const bool s2 = !env_is("FRACTAL_S2", "0");
   if constexpr (NC == 1 && std::is_same<T, float>::value && !STRICT) {
     if (s2 && g.counts8 == nullptr) {
-      const int64_t tiles2 = (int64_t)g.tiles_x * ((g.rows + 2 * fr::kTileH - 1) / (2 * fr::kTileH));
+      const dim3 grid2 = tile_grid(g, (g.rows + 2 * fr::kTileH - 1) / (2 * fr::kTileH), 1);
       fr::escape_tile2_kernel<MANDEL, COLOR>
-          <<<dim3((unsigned)tiles2, 1, 1), fr::kThreads, 0, s>>>(g, pal, cs.re[0], cs.im[0]);
+          <<<grid2, fr::kThreads, 0, s>>>(g, pal, cs.re[0], cs.im[0]);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return cudaGetLastError();
     }
   }
+  const dim3 grid = tile_grid(g, (g.rows + fr::kTileH - 1) / fr::kTileH, (n_frames + fpc - 1) / fpc);
   constexpr int KD = sizeof(T) == 8 ? 2 * kStaticK : kStaticK;
   if (g.counts8 != nullptr) {  // uint8 counts: path chunks only (julia_render_path8)
     if constexpr (NC > 1 && !MANDEL)
@@ -514,13 +523,14 @@ fr_status render_frame(bool mandel, fr_complex c, fr_window win, int32_t width, 
 }
 
 template <class T, int FN, bool COLOR>
-cudaError_t launch_fn_t(const fr::Geom& g, const fr::Palette& pal, fr_complex c, cudaStream_t s) {
+cudaError_t launch_fn_t(const fr::Geom& g0, const fr::Palette& pal, fr_complex c, cudaStream_t s) {
+  fr::Geom g = g0;
   fr::CList<T, 1> cs;
   cs.re[0] = state_of<T, true>(c.re);
   cs.im[0] = state_of<T, true>(c.im);
-  const int64_t tiles = (int64_t)g.tiles_x * ((g.rows + fr::kTileH - 1) / fr::kTileH);
+  const dim3 grid = tile_grid(g, (g.rows + fr::kTileH - 1) / fr::kTileH, 1);
   fr::escape_tile_kernel<T, true, false, COLOR, 4, 1, FN>
-      <<<dim3((unsigned)tiles, 1, 1), fr::kThreads, 0, s>>>(g, pal, cs, 0, 1, 1);
+      <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, 0, 1, 1);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

@@ -166,6 +166,35 @@ def test_largest_frame(fr):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("mode", ["FP32_STRICT", "FP32_FAST", "FP64_STRICT"])
+def test_tall_frame_linear_grid(fr, mode):
+    """More than 65535 tile rows: kernels S/S2 fall back from the (x, y[, z]) grid to
+    linear tiles with a division (tile_of), with a ragged 37-pixel width.  Strict modes
+    (kernel S) are bit-exact on sampled pixels; fast mode (kernel S2, no bit-exact
+    oracle) must write every pixel and agree with the strict fp32 oracle on >= 99% of
+    the sample -- a tile-mapping error would scramble whole tiles."""
+    w, h = 37, 1_100_000  # S: 137,500 tile rows; S2: 68,750 (both > 65535)
+    m = fr.Mode[mode]
+    out = torch.full((h, w), -1, dtype=torch.int16, device="cuda").view(torch.uint16)
+    win = W.julia_window(w, h, span_re=1.0e-4)  # half_h = 1.49: a thin column through the set
+    c = -0.8 + 0.156j
+    fr.julia_render_ex(c, win, w, h, 60, m, out=out)
+    torch.cuda.synchronize()
+    assert not bool((out.view(torch.int16) == -1).any())
+    rng = np.random.default_rng(2)
+    px = np.r_[0, w - 1, 0, w - 1, rng.integers(0, w, 3000)]
+    py = np.r_[0, 0, h - 1, h - 1, rng.integers(0, h, 3000)]
+    got = sample16(out, py, px)
+    prec = 64 if mode.startswith("FP64") else 32
+    ref = oracle.pixels("julia", c, win.center, win.half_w, win.half_h, w, h, 60, prec, px, py)
+    if mode == "FP32_FAST":
+        assert np.mean(got != ref) <= 0.01
+    else:
+        np.testing.assert_array_equal(got, ref)
+    del out
+    torch.cuda.empty_cache()
+
+
 # ------------------------------------------------------------------ paths (cfg4)
 def test_path_equals_single_frames(fr):
     """julia_render_path(C[])[k] == julia_render_ex(C[k]) byte-exactly, across the
