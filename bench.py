@@ -443,12 +443,28 @@ def measure_e2e(fr, W, cs, win, world, args, barrier, stream):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     iters = int(host.numpy().sum(dtype=np.int64))
+    # roofline of e2e: a plain pinned device->host copy of the same bytes (torch)
+    dev = torch.empty((nf, H_PX, W_PX), dtype=torch.uint8, device="cuda")
+    host.copy_(dev, non_blocking=True)
+    torch.cuda.synchronize()
+    c0 = torch.cuda.Event(enable_timing=True)
+    c1 = torch.cuda.Event(enable_timing=True)
+    c0.record()
+    host.copy_(dev, non_blocking=True)
+    c1.record()
+    torch.cuda.synchronize()
+    copy_gbs = dev.numel() / (c0.elapsed_time(c1) * 1e-3) / 1e9
+    del dev
     tot = torch.tensor([float(iters)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
     return {"value": float(tot.item()) * steps / (ms * 1e-3) / 1e9, "unit": "Gpixel-iter/s",
             "h2d_bytes_per_step": int(nf * 16), "d2h_bytes_per_step": int(nf * H_PX * W_PX),
             "steps": steps, "ms_per_step": ms / steps,
+            "d2h_GB_per_s": nf * H_PX * W_PX / (ms / steps * 1e-3) / 1e9,
+            "d2h_copy_peak_GB_per_s": copy_gbs,
+            "bound": "PCIe device->host: d2h_copy_peak_GB_per_s is one plain pinned copy of "
+                     "the same bytes (torch), measured in this run",
             "api": "julia_render_path_host (C ABI, host output buffer)",
             "note": "C values (16 B/frame) host->device as kernel parameters; uint8 counts "
                     "device->host into pinned memory inside the call, 128 MiB chunks "

@@ -713,6 +713,217 @@ escape_tile2_kernel(const Geom g, const Palette pal, const float jcr2, const flo
   }
 }
 
+// Optional per-warp timeline of kernels R and P2 (diagnostics; null in normal operation):
+// [warp][0] = %globaltimer at entry, [1] = at chunk-supply exhaustion, [2] = at exit.
+__device__ unsigned long long* g_refill_trace = nullptr;
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ----------------------------------------------------------------------------------
+// Two-phase rendering of heavy-tailed single frames (kernels P1 + P2).  Most pixels of a
+// heavy-tailed frame escape within a few iterations (cfg3: p50 = 2) while most of the
+// WORK is in the few long orbits (cfg3: 20% of pixels survive 32 iterations and carry 83%
+// of the iterations).  One kernel serves both badly: small vote blocks waste issue on the
+// long orbits, large refill blocks waste most of a block on every short one.
+//   P1: static 8x4 warp tiles, vote blocks of 4, stop at a budget of B iterations.
+//       Pixels that escaped store their count (and colour); survivors append their
+//       state (Z_B, B, pixel index) to a queue -- aggregated per CTA, one global atomic
+//       per CTA.
+//   P2: persistent lane refill over the queue (blocks of K, service threshold TH):
+//       warps take 32 items per atomic, the next grab prefetched.  The orbit continues
+//       from Z_B with the same arithmetic, so counts are bit-identical to one pass.
+// ----------------------------------------------------------------------------------
+template <class T>
+struct QItem {
+  T x, y;        // state after the phase-1 budget (kernel representation)
+  int cnt;       // iterations done (= the budget)
+  unsigned idx;  // pixel index row * W + px within the call's rows
+};
+
+struct ContQueue {
+  unsigned tail;  // items appended by P1 (its survivors)
+  unsigned pad0[31];
+  unsigned head;  // items taken by P2
+  unsigned pad1[31];
+  unsigned done_warps;
+  unsigned pad2[31];
+};
+
+template <class T, bool STRICT, bool MANDEL, bool COLOR>
+__global__ void __launch_bounds__(kThreads)
+escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, int budget,
+                     ContQueue* q, QItem<T>* items) {
+  __shared__ uchar4 spal[COLOR ? 256 : 1];
+  __shared__ unsigned s_n, s_base;
+  int tx, ty, grp;
+  tile_of(g, tx, ty, grp);
+  if (threadIdx.x == 0) s_n = 0u;
+  if (COLOR) spal[threadIdx.x] = pal.e[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int px = tx * kTileW + (warp & 3) * kWarpW + (lane & 7);
+  const int ly = ty * kTileH + (warp >> 2) * kWarpH + (lane >> 3);
+  const bool inside = (px < g.W) && (ly < g.rows);
+  const T are = to_state<T, STRICT>(pixel_re(g, min(px, g.W - 1)));
+  const T aim = to_state<T, STRICT>(pixel_im(g, global_row(g, min(ly, g.rows - 1))));
+  T x, y, cr, ci;
+  if (MANDEL) {
+    x = y = T(0);
+    cr = are;
+    ci = aim;
+  } else {
+    x = are;
+    y = aim;
+    cr = jcr;
+    ci = jci;
+  }
+  unsigned alive = inside ? 1u : 0u;
+  int cnt = 0;
+  // budget is a multiple of 4 and < max_iter (host)
+  if constexpr (kAsmLoop<T, STRICT, 4>) {
+    fast_vote_loop_f32<4>(x, y, cnt, alive, cr, ci, budget);
+  } else {
+    for (int n = 0; n < budget; n += 4) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
+      if (!__any_sync(kFull, alive)) break;
+    }
+  }
+  const bool surv = inside && alive;  // |Z_n|^2 <= 4 for every n < budget
+  const unsigned idx = (unsigned)ly * (unsigned)g.W + (unsigned)px;
+  if (inside && !surv) {
+    g.counts[idx] = (uint16_t)cnt;
+    if (COLOR) g.rgba[idx] = colour_of(spal, pal, cnt, g.max_iter);
+  }
+  // CTA-aggregated append of the survivors
+  const unsigned b = __ballot_sync(kFull, surv);
+  unsigned wbase = 0u;
+  if (lane == 0 && b) wbase = atomicAdd(&s_n, (unsigned)__popc(b));
+  __syncthreads();
+  if (threadIdx.x == 0 && s_n) s_base = atomicAdd(&q->tail, s_n);
+  __syncthreads();
+  wbase = __shfl_sync(kFull, wbase, 0);
+  if (surv) {
+    QItem<T> it;
+    it.x = x;
+    it.y = y;
+    it.cnt = cnt;
+    it.idx = idx;
+    items[s_base + wbase + (unsigned)__popc(b & ((1u << lane) - 1u))] = it;
+  }
+}
+
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH>
+__global__ void __launch_bounds__(kThreads)
+escape_cont_kernel(const Geom g, const Palette pal, const T jcr, const T jci, ContQueue* q,
+                   const QItem<T>* items) {
+  __shared__ uchar4 spal[COLOR ? 256 : 1];
+  if (COLOR) {
+    spal[threadIdx.x] = pal.e[threadIdx.x];
+    __syncthreads();
+  }
+  using It = Iter<T, STRICT>;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int max_iter = g.max_iter;
+  const unsigned n_items = *reinterpret_cast<volatile unsigned*>(&q->tail);
+  unsigned long long* trace = g_refill_trace;
+  const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (trace && lane == 0) trace[gw * 3] = global_ns();
+  bool exhausted = false;
+  unsigned need = kFull;
+  unsigned gpos = 32u, gend = 0u;  // current grab [gpos, gend) of item positions
+  unsigned pf = 0u;                // lane 0: prefetched grab base
+  bool have_pf = false;
+
+  T x = T(0), y = T(0), cr = jcr, ci = jci;
+  unsigned alive = 0u;
+  int cnt = 0;
+  int64_t off = -1;
+
+  for (;;) {
+    while (need != 0u && !exhausted) {
+      if (gpos >= gend) {
+        unsigned base = 0u;
+        if (lane == 0) base = have_pf ? pf : atomicAdd(&q->head, 32u);
+        base = __shfl_sync(kFull, base, 0);
+        have_pf = false;
+        if (base >= n_items) {
+          exhausted = true;
+          if (trace && lane == 0) trace[gw * 3 + 1] = global_ns();
+          break;
+        }
+        gpos = base;
+        gend = min(base + 32u, n_items);
+        if (lane == 0 && gend < n_items) pf = atomicAdd(&q->head, 32u);
+        have_pf = gend < n_items;
+      }
+      const unsigned avail = gend - gpos;
+      const unsigned rank = (unsigned)__popc(need & lt_mask);
+      const bool mine = (need >> lane) & 1u;
+      bool got = false;
+      if (mine && rank < avail) {
+        const QItem<T> it = items[gpos + rank];
+        got = true;
+        off = it.idx;
+        x = it.x;
+        y = it.y;
+        cnt = it.cnt;
+        alive = 1u;
+        if (MANDEL) {
+          const int row = (int)(it.idx / (unsigned)g.W);
+          const int px = (int)(it.idx - (unsigned)row * (unsigned)g.W);
+          cr = to_state<T, STRICT>(pixel_re(g, px));
+          ci = to_state<T, STRICT>(pixel_im(g, global_row(g, row)));
+        }
+      }
+      const unsigned nneed = (unsigned)__popc(need);
+      gpos += nneed < avail ? nneed : avail;
+      need = __ballot_sync(kFull, mine && !got);
+    }
+    const int n_held = __popc(__ballot_sync(kFull, off >= 0));
+    if (n_held == 0) break;
+    const bool held = off >= 0;
+    const int thr = exhausted ? 1 : (TH < n_held ? TH : n_held);
+    const int lim = held ? max_iter : 0x7fffffff;
+    if (!held) alive = 0u;
+    bool fin;
+    unsigned fm;
+    for (;;) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) It::step(x, y, cr, ci, alive, cnt);
+      fin = held && (!alive || cnt >= lim);
+      fm = __ballot_sync(kFull, fin);
+      if (__popc(fm) >= thr) break;
+    }
+    if (fin) {
+      const int count = cnt < max_iter ? cnt : max_iter;
+      g.counts[off] = (uint16_t)count;
+      if (COLOR) g.rgba[off] = colour_of(spal, pal, count, max_iter);
+      off = -1;
+      alive = 0u;
+    }
+    need = fm;
+  }
+  if (trace && lane == 0) trace[gw * 3 + 2] = global_ns();
+  // ---- self-reset of the queue by the last warp to finish
+  if (lane == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&q->done_warps, 1u);
+    if (prev == gridDim.x * (kThreads / 32) - 1) {
+      q->tail = 0u;
+      q->head = 0u;
+      q->done_warps = 0u;
+      __threadfence();
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------------
 // Persistent lane-refill kernel (R) for one frame whose counts are heavy-tailed or long
 // (SURVEY §7 hard part 1).  Each warp owns a 32x8-pixel chunk at a time, taken from a
@@ -730,16 +941,6 @@ escape_tile2_kernel(const Geom g, const Palette pal, const float jcr2, const flo
 //   with |Z_n|^2 > 4 satisfies |Z_{n+1}| >= |Z_n|^2 - |C| - err > 2 forever after
 //   (DESIGN.md "Escape-monotonicity lemma"), so the block-end test cannot miss an escape.
 // ----------------------------------------------------------------------------------
-// Optional per-warp timeline of kernel R (diagnostics; null in normal operation):
-// [warp][0] = %globaltimer at entry, [1] = at chunk-supply exhaustion, [2] = at exit.
-__device__ unsigned long long* g_refill_trace = nullptr;
-
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
 struct Workspace {
   unsigned int next_chunk;
   unsigned int done_warps;

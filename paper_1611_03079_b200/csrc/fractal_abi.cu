@@ -365,6 +365,78 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
   return cudaGetLastError();
 }
 
+// Two-phase kernels P1 + P2: the queue header (zeroed once per (device, stream), reset by
+// P2's last warp) and an item buffer of one QItem per pixel of the call, grown on demand.
+std::map<std::pair<int, uintptr_t>, std::pair<void*, size_t>> g_queue, g_items;
+constexpr int64_t kTwoPhaseMaxPixels = int64_t(1) << 25;  // item buffer <= 1 GiB (fp64)
+
+int twophase_budget() {  // FRACTAL_BUDGET (multiple of 4), default 128
+  static const int b = [] {
+    const int v = env_int("FRACTAL_BUDGET", 128);
+    return v < 4 ? 4 : v - v % 4;
+  }();
+  return b;
+}
+
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH>
+cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double2 c,
+                              cudaStream_t s) {
+  fr::Geom g = g0;
+  const T jcr = MANDEL ? T(0) : state_of<T, STRICT>(c.x);
+  const T jci = MANDEL ? T(0) : state_of<T, STRICT>(c.y);
+  const int64_t n = (int64_t)g.rows * g.W;
+  void* qp = nullptr;
+  bool fresh = false;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_ws_mutex);
+    fresh = g_queue.find(std::make_pair(dev, (uintptr_t)s)) == g_queue.end();
+  }
+  cudaError_t e = buffer_for(g_queue, s, sizeof(fr::ContQueue), &qp);
+  if (e != cudaSuccess) return e;
+  if (fresh && (e = cudaMemset(qp, 0, sizeof(fr::ContQueue))) != cudaSuccess) return e;
+  auto* q = static_cast<fr::ContQueue*>(qp);
+  void* ip = nullptr;
+  e = buffer_for(g_items, s, (size_t)n * sizeof(fr::QItem<T>), &ip);
+  if (e != cudaSuccess) return e;
+  auto* items = static_cast<fr::QItem<T>*>(ip);
+  const dim3 grid1 = tile_grid(g, (g.rows + fr::kTileH - 1) / fr::kTileH, 1);
+  fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR>
+      <<<grid1, fr::kThreads, 0, s>>>(g, pal, jcr, jci, twophase_budget(), q, items);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  auto kern = fr::escape_cont_kernel<T, STRICT, MANDEL, COLOR, K, TH>;
+  static const int occ = [&] {
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, fr::kThreads, 0) != cudaSuccess ||
+        o <= 0)
+      o = 1;
+    return o;
+  }();
+  // P2 runs 3 CTAs per SM (FRACTAL_P2_OCC), not the occupancy limit: ~3 warps per SMSP
+  // already saturate issue for this loop, and every extra resident lane only adds to the
+  // work still in flight when the queue runs dry (cfg3: 8 CTAs 0.273 ms, 3 CTAs 0.228)
+  static const int occ_env = env_int("FRACTAL_P2_OCC", 3);
+  const int occ2 = occ_env > 0 && occ_env < occ ? occ_env : occ;
+  kern<<<(unsigned)(sm_count() * occ2), fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+template <bool MANDEL, bool COLOR>
+cudaError_t launch_twophase_mode(fr_mode mode, const fr::Geom& g, const fr::Palette& pal,
+                                 double2 c, cudaStream_t s) {
+  switch (mode) {
+    case FR_FP32_FAST: return launch_twophase_t<float, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
+    case FR_FP32_STRICT: return launch_twophase_t<float, true, MANDEL, COLOR, 16, 8>(g, pal, c, s);
+    case FR_FP64_FAST: return launch_twophase_t<double, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
+    case FR_FP64_STRICT: return launch_twophase_t<double, true, MANDEL, COLOR, 16, 8>(g, pal, c, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 // Tuning variants of the refill kernel for FP32_FAST (FRACTAL_REFILL=K,TH); default 16,8.
 int refill_variant() {
   static const int v = [] {
@@ -460,20 +532,23 @@ bool monotone_ok(bool mandel, fr_complex c, fr_window w) {
 
 // Scheduling policy for single frames: FRACTAL_SCHED=static|refill overrides; default
 // refill for max_iter >= 256 (heavy-tailed counts), static otherwise.
-enum Sched { kStatic = 0, kRefill = 1, kAmort = 2 };
+enum Sched { kStatic = 0, kRefill = 1, kAmort = 2, kTwoPhase = 3 };
 
 Sched choose_sched(bool mandel, fr_complex c, fr_window w, int max_iter) {
   static const int forced = env_is("FRACTAL_SCHED", "static")   ? kStatic
                             : env_is("FRACTAL_SCHED", "refill") ? kRefill
                             : env_is("FRACTAL_SCHED", "amort")  ? kAmort
+                            : env_is("FRACTAL_SCHED", "twophase") ? kTwoPhase
                                                                  : -1;
   const bool mono = monotone_ok(mandel, c, w);
   if (forced >= 0) return (forced == kAmort && !mono) ? kRefill : (Sched)forced;
   if (max_iter < 256) return kStatic;
   // Long, low-divergence counts (deep Mandelbrot zooms) amortise the escape test;
-  // heavy-tailed Julia frames keep the exact per-iteration test with lane refill.
+  // heavy-tailed frames keep the exact per-iteration test: a budgeted static pass then
+  // lane refill over its survivors (P1 + P2), or plain lane refill (R) when the frame
+  // is too large for the survivor buffer.
   if (mandel && mono && max_iter >= 1000) return kAmort;
-  return kRefill;
+  return kTwoPhase;
 }
 
 bool mode_valid(fr_mode m) {
@@ -508,6 +583,14 @@ fr_status render_frame(bool mandel, fr_complex c, fr_window win, int32_t width, 
       else
         e = col ? launch_amort_mode<false, true>(mode, g, p, cc, stream)
                 : launch_amort_mode<false, false>(mode, g, p, cc, stream);
+    } else if (sched == kTwoPhase && max_iter > twophase_budget() &&
+               (int64_t)g.rows * g.W <= kTwoPhaseMaxPixels) {
+      if (mandel)
+        e = col ? launch_twophase_mode<true, true>(mode, g, p, cc, stream)
+                : launch_twophase_mode<true, false>(mode, g, p, cc, stream);
+      else
+        e = col ? launch_twophase_mode<false, true>(mode, g, p, cc, stream)
+                : launch_twophase_mode<false, false>(mode, g, p, cc, stream);
     } else if (mandel) {
       e = col ? launch_refill_mode<true, true>(mode, g, p, cc, stream)
               : launch_refill_mode<true, false>(mode, g, p, cc, stream);

@@ -1,6 +1,7 @@
 """Every kernel family, whatever the default dispatch picks: a parity subset re-run in
-subprocesses with FRACTAL_SCHED forced to static (kernel S), refill (kernel R) and
-amort (kernel A), and with the persistent / CTA-local refill grids."""
+subprocesses with FRACTAL_SCHED forced to static (kernel S), refill (kernel R), amort
+(kernel A) and twophase (kernels P1 + P2, at several phase-1 budgets), and with the
+persistent / CTA-local refill grids."""
 import os
 import subprocess
 import sys
@@ -15,7 +16,10 @@ SUBSET = ("test_strict_configs_full_frame or test_strict_fuzz or test_strict_rag
 
 
 @pytest.mark.parametrize("env", [{"FRACTAL_SCHED": "static"}, {"FRACTAL_SCHED": "refill"},
-                                 {"FRACTAL_SCHED": "amort"},
+                                 {"FRACTAL_SCHED": "amort"}, {"FRACTAL_SCHED": "twophase"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_BUDGET": "4"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_BUDGET": "48",
+                                  "FRACTAL_P2_OCC": "1"},
                                  {"FRACTAL_SCHED": "refill", "FRACTAL_REFILL_CPC": "16"},
                                  {"FRACTAL_SCHED": "refill", "FRACTAL_CONT": "1"},
                                  {"FRACTAL_SCHED": "amort", "FRACTAL_REFILL_CPC": "0"}])
