@@ -25,6 +25,8 @@ struct Palette {
   uchar4 interior;
   uint32_t n;      // entries, 2..256
   uint32_t magic;  // ceil(2^32 / n): count mod n = c - n * umulhi(c, magic) for c < 2^16
+  const uchar4* dev;  // the n entries in device memory (short-lived CTAs read it through
+                      // L1 instead of staging e[] in shared memory behind a CTA barrier)
 };
 
 struct Geom {
@@ -318,6 +320,14 @@ __device__ __forceinline__ uchar4 colour_of(const uchar4* spal, const Palette& p
   const unsigned c = (unsigned)cnt;
   const unsigned q = __umulhi(c, p.magic);
   return spal[c - q * p.n];
+}
+
+// The same colour level from the device copy of the palette (read-only path).
+__device__ __forceinline__ uchar4 colour_dev(const Palette& p, int cnt, int max_iter) {
+  if (cnt == max_iter) return p.interior;
+  const unsigned c = (unsigned)cnt;
+  const unsigned q = __umulhi(c, p.magic);
+  return __ldg(p.dev + (c - q * p.n));
 }
 
 // ----------------------------------------------------------------------------------
@@ -654,13 +664,9 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
 template <bool MANDEL, bool COLOR>
 __global__ void __launch_bounds__(kThreads)
 escape_tile2_kernel(const Geom g, const Palette pal, const float jcr2, const float jci2) {
-  __shared__ uchar4 spal[COLOR ? 256 : 1];
+  // colours from the device palette (no CTA barrier in these short-lived CTAs)
   int tx, ty, grp;
   tile_of(g, tx, ty, grp);
-  if (COLOR) {
-    spal[threadIdx.x] = pal.e[threadIdx.x];
-    __syncthreads();
-  }
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int cx = (warp & 3) * kWarpW + (lane & 7);
@@ -703,13 +709,13 @@ escape_tile2_kernel(const Geom g, const Palette pal, const float jcr2, const flo
     const int64_t off = (int64_t)ly0 * g.W + px;
     const int c0 = cnt;  // <= max_iter: at most one increment per executed iteration
     g.counts[off] = (uint16_t)c0;
-    if (COLOR) g.rgba[off] = colour_of(spal, pal, c0, max_iter);
+    if (COLOR) g.rgba[off] = colour_dev(pal, c0, max_iter);
   }
   if (in1) {
     const int64_t off = (int64_t)ly1 * g.W + px;
     const int c1 = cnt2;
     g.counts[off] = (uint16_t)c1;
-    if (COLOR) g.rgba[off] = colour_of(spal, pal, c1, max_iter);
+    if (COLOR) g.rgba[off] = colour_dev(pal, c1, max_iter);
   }
 }
 
@@ -729,10 +735,10 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // WORK is in the few long orbits (cfg3: 20% of pixels survive 32 iterations and carry 83%
 // of the iterations).  One kernel serves both badly: small vote blocks waste issue on the
 // long orbits, large refill blocks waste most of a block on every short one.
-//   P1: static 8x4 warp tiles, vote blocks of 4, stop at a budget of B iterations.
+//   P1: static tiles, two pixels per thread (the S2 layout), vote blocks of 4, stop at a
+//       budget of B iterations.
 //       Pixels that escaped store their count (and colour); survivors append their
-//       state (Z_B, B, pixel index) to a queue -- aggregated per CTA, one global atomic
-//       per CTA.
+//       state (Z_B, B, pixel index) to a queue, one atomic per warp that has any.
 //   P2: persistent lane refill over the queue (blocks of K, service threshold TH):
 //       warps take 32 items per atomic, the next grab prefetched.  The orbit continues
 //       from Z_B with the same arithmetic, so counts are bit-identical to one pass.
@@ -757,64 +763,87 @@ template <class T, bool STRICT, bool MANDEL, bool COLOR>
 __global__ void __launch_bounds__(kThreads)
 escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, int budget,
                      ContQueue* q, QItem<T>* items) {
-  __shared__ uchar4 spal[COLOR ? 256 : 1];
-  __shared__ unsigned s_n, s_base;
+  // CTA tile 32x16: each thread iterates the pixels of rows ly and ly + 8 of its 8x4-lane
+  // warp tile together (two orbits, one vote per block of 4; the S2 layout).  Colours come
+  // from the device palette: no CTA barrier in these short-lived CTAs.
   int tx, ty, grp;
   tile_of(g, tx, ty, grp);
-  if (threadIdx.x == 0) s_n = 0u;
-  if (COLOR) spal[threadIdx.x] = pal.e[threadIdx.x];
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int px = tx * kTileW + (warp & 3) * kWarpW + (lane & 7);
-  const int ly = ty * kTileH + (warp >> 2) * kWarpH + (lane >> 3);
-  const bool inside = (px < g.W) && (ly < g.rows);
-  const T are = to_state<T, STRICT>(pixel_re(g, min(px, g.W - 1)));
-  const T aim = to_state<T, STRICT>(pixel_im(g, global_row(g, min(ly, g.rows - 1))));
-  T x, y, cr, ci;
+  const int ly0 = ty * (2 * kTileH) + (warp >> 2) * kWarpH + (lane >> 3);
+  const int ly1 = ly0 + kTileH;
+  const bool in0 = (px < g.W) && (ly0 < g.rows);
+  const bool in1 = (px < g.W) && (ly1 < g.rows);
+  const T re = to_state<T, STRICT>(pixel_re(g, min(px, g.W - 1)));
+  const T im0 = to_state<T, STRICT>(pixel_im(g, global_row(g, min(ly0, g.rows - 1))));
+  const T im1 = to_state<T, STRICT>(pixel_im(g, global_row(g, min(ly1, g.rows - 1))));
+  T x, y, x2, y2, cr, ci, cr2, ci2;
   if (MANDEL) {
-    x = y = T(0);
-    cr = are;
-    ci = aim;
+    x = y = x2 = y2 = T(0);
+    cr = re;
+    ci = im0;
+    cr2 = re;
+    ci2 = im1;
   } else {
-    x = are;
-    y = aim;
-    cr = jcr;
-    ci = jci;
+    x = re;
+    y = im0;
+    x2 = re;
+    y2 = im1;
+    cr = cr2 = jcr;
+    ci = ci2 = jci;
   }
-  unsigned alive = inside ? 1u : 0u;
-  int cnt = 0;
+  unsigned alive = in0 ? 1u : 0u, alive2 = in1 ? 1u : 0u;
+  int cnt = 0, cnt2 = 0;
   // budget is a multiple of 4 and < max_iter (host)
   if constexpr (kAsmLoop<T, STRICT, 4>) {
-    fast_vote_loop_f32<4>(x, y, cnt, alive, cr, ci, budget);
+    fast_vote_loop2_f32<4>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2, budget);
   } else {
     for (int n = 0; n < budget; n += 4) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
-      if (!__any_sync(kFull, alive)) break;
+      for (int j = 0; j < 4; ++j) {
+        Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
+        Iter<T, STRICT>::step(x2, y2, cr2, ci2, alive2, cnt2);
+      }
+      if (!__any_sync(kFull, alive | alive2)) break;
     }
   }
-  const bool surv = inside && alive;  // |Z_n|^2 <= 4 for every n < budget
-  const unsigned idx = (unsigned)ly * (unsigned)g.W + (unsigned)px;
-  if (inside && !surv) {
-    g.counts[idx] = (uint16_t)cnt;
-    if (COLOR) g.rgba[idx] = colour_of(spal, pal, cnt, g.max_iter);
+  // |Z_n|^2 <= 4 for every n < budget: survivor; else the count is final
+  const bool s0 = in0 && alive, s1 = in1 && alive2;
+  const unsigned i0 = (unsigned)ly0 * (unsigned)g.W + (unsigned)px;
+  const unsigned i1 = (unsigned)ly1 * (unsigned)g.W + (unsigned)px;
+  if (in0 && !s0) {
+    g.counts[i0] = (uint16_t)cnt;
+    if (COLOR) g.rgba[i0] = colour_dev(pal, cnt, g.max_iter);
   }
-  // CTA-aggregated append of the survivors
-  const unsigned b = __ballot_sync(kFull, surv);
-  unsigned wbase = 0u;
-  if (lane == 0 && b) wbase = atomicAdd(&s_n, (unsigned)__popc(b));
-  __syncthreads();
-  if (threadIdx.x == 0 && s_n) s_base = atomicAdd(&q->tail, s_n);
-  __syncthreads();
-  wbase = __shfl_sync(kFull, wbase, 0);
-  if (surv) {
-    QItem<T> it;
-    it.x = x;
-    it.y = y;
-    it.cnt = cnt;
-    it.idx = idx;
-    items[s_base + wbase + (unsigned)__popc(b & ((1u << lane) - 1u))] = it;
+  if (in1 && !s1) {
+    g.counts[i1] = (uint16_t)cnt2;
+    if (COLOR) g.rgba[i1] = colour_dev(pal, cnt2, g.max_iter);
+  }
+  // append the survivors: one atomic per warp that has any (no CTA barrier, so a warp
+  // that finished early never waits for the CTA's slowest)
+  const unsigned b0 = __ballot_sync(kFull, s0), b1 = __ballot_sync(kFull, s1);
+  if (b0 | b1) {
+    unsigned base = 0u;
+    if (lane == 0) base = atomicAdd(&q->tail, (unsigned)(__popc(b0) + __popc(b1)));
+    base = __shfl_sync(kFull, base, 0);
+    const unsigned lt = (1u << lane) - 1u;
+    if (s0) {
+      QItem<T> it;
+      it.x = x;
+      it.y = y;
+      it.cnt = cnt;
+      it.idx = i0;
+      items[base + (unsigned)__popc(b0 & lt)] = it;
+    }
+    if (s1) {
+      QItem<T> it;
+      it.x = x2;
+      it.y = y2;
+      it.cnt = cnt2;
+      it.idx = i1;
+      items[base + (unsigned)__popc(b0) + (unsigned)__popc(b1 & lt)] = it;
+    }
   }
 }
 

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <vector>
 #include <mutex>
 #include <new>
 #include <utility>
@@ -84,6 +85,50 @@ fr_status make_palette(const fr_palette* pal, fr::Palette* out) {
   out->n = (uint32_t)pal->n;
   out->magic = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)pal->n - 1) / (uint64_t)pal->n);
   return FR_OK;
+}
+
+// Device copies of palettes, cached per device by content (a 64-bit hash, confirmed by
+// comparing the entries): kernels S2 and P1 read colours through L1 instead of staging
+// the palette in shared memory behind a CTA barrier.  A new palette is uploaded once,
+// outside any graph capture (like the workspaces).
+struct DevPalette {
+  std::vector<uchar4> entries;
+  uchar4* ptr;
+};
+std::mutex g_pal_mutex;
+std::map<std::pair<int, uint64_t>, std::vector<DevPalette>> g_pal_dev;
+
+bool capturing(cudaStream_t s);
+
+cudaError_t device_palette(fr::Palette& p, cudaStream_t s) {
+  p.dev = nullptr;
+  if (p.n == 0) return cudaSuccess;
+  uint64_t h = 1469598103934665603ull;  // FNV-1a over the entries
+  for (uint32_t i = 0; i < p.n; ++i) {
+    const uchar4 v = p.e[i];
+    for (unsigned char b : {v.x, v.y, v.z, v.w}) h = (h ^ b) * 1099511628211ull;
+  }
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(g_pal_mutex);
+  auto& bucket = g_pal_dev[std::make_pair(dev, h)];
+  for (const DevPalette& d : bucket) {
+    if (d.entries.size() == p.n &&
+        std::memcmp(d.entries.data(), p.e, p.n * sizeof(uchar4)) == 0) {
+      p.dev = d.ptr;
+      return cudaSuccess;
+    }
+  }
+  if (capturing(s)) return cudaErrorStreamCaptureUnsupported;
+  uchar4* ptr = nullptr;
+  e = cudaMalloc(&ptr, p.n * sizeof(uchar4));
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpy(ptr, p.e, p.n * sizeof(uchar4), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return e;
+  bucket.push_back(DevPalette{std::vector<uchar4>(p.e, p.e + p.n), ptr});
+  p.dev = ptr;
+  return cudaSuccess;
 }
 
 // Parameter derivation in binary64: hx = half_w / W, hy = half_h / H.
@@ -370,9 +415,9 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
 std::map<std::pair<int, uintptr_t>, std::pair<void*, size_t>> g_queue, g_items;
 constexpr int64_t kTwoPhaseMaxPixels = int64_t(1) << 25;  // item buffer <= 1 GiB (fp64)
 
-int twophase_budget() {  // FRACTAL_BUDGET (multiple of 4), default 128
+int twophase_budget() {  // FRACTAL_BUDGET (multiple of 4), default 96
   static const int b = [] {
-    const int v = env_int("FRACTAL_BUDGET", 128);
+    const int v = env_int("FRACTAL_BUDGET", 96);
     return v < 4 ? 4 : v - v % 4;
   }();
   return b;
@@ -401,7 +446,7 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   e = buffer_for(g_items, s, (size_t)n * sizeof(fr::QItem<T>), &ip);
   if (e != cudaSuccess) return e;
   auto* items = static_cast<fr::QItem<T>*>(ip);
-  const dim3 grid1 = tile_grid(g, (g.rows + fr::kTileH - 1) / fr::kTileH, 1);
+  const dim3 grid1 = tile_grid(g, (g.rows + 2 * fr::kTileH - 1) / (2 * fr::kTileH), 1);
   fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR>
       <<<grid1, fr::kThreads, 0, s>>>(g, pal, jcr, jci, twophase_budget(), q, items);
   e = cudaGetLastError();
@@ -572,6 +617,7 @@ fr_status render_frame(bool mandel, fr_complex c, fr_window win, int32_t width, 
   if ((pal != nullptr) != (out_rgba != nullptr)) return FR_ERR_INVALID_ARG;
   const fr::Geom g = make_geom(win, width, height, max_iter, bands, rows, out_counts, out_rgba);
   cudaError_t e;
+  if (pal != nullptr && (e = device_palette(p, stream)) != cudaSuccess) return cuda_status(e);
   const Sched sched = choose_sched(mandel, c, win, max_iter);
   if (sched != kStatic) {
     const double2 cc = make_double2(c.re, c.im);

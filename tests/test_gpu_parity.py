@@ -291,15 +291,33 @@ def test_colorize_standalone(fr, n, offset):
     np.testing.assert_array_equal(got.cpu().numpy(), oracle.colorize(counts[offset:], 1000, *odd))
 
 
-def test_fused_colorize_matches_standalone(fr):
-    cfg = W.configs()["cfg2"]
-    pal = W.palette("fire")
+@pytest.mark.parametrize("name,mode,pal_name", [("cfg2", "FP32_FAST", "fire"),
+                                               ("cfg3", "FP32_FAST", "classic"),
+                                               ("cfg3", "FP64_STRICT", "fire")])
+def test_fused_colorize_matches_standalone(fr, name, mode, pal_name):
+    """Fused colour levels (S2 at max_iter < 256, P1 + P2 above; palettes read from the
+    device copy or shared memory) equal the standalone colorize of the same counts."""
+    cfg = W.configs()[name]
+    pal = W.palette(pal_name)
     counts, rgba = gpu_julia(fr, cfg.c, cfg.window, cfg.width, cfg.height, cfg.max_iter,
-                             fr.Mode.FP32_FAST, palette=pal)
+                             fr.Mode[mode], palette=pal)
     t = torch.from_numpy(counts.view(np.int16)).cuda().view(torch.uint16)
     again = fr.colorize(t, cfg.max_iter, pal)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(again.cpu().numpy(), rgba)
+
+
+def test_two_palettes_alternating(fr):
+    """The device palette cache keys on content: alternating palettes never mix."""
+    cfg = W.configs()["cfg2"]
+    for pal_name in ("fire", "classic", "fire"):
+        pal = W.palette(pal_name)
+        counts, rgba = gpu_julia(fr, cfg.c, cfg.window, 480, 270, cfg.max_iter,
+                                 fr.Mode.FP32_FAST, palette=pal)
+        t = torch.from_numpy(counts.view(np.int16)).cuda().view(torch.uint16)
+        again = fr.colorize(t, cfg.max_iter, pal)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(again.cpu().numpy(), rgba)
 
 
 # ------------------------------------------------------------------ fast-mode tolerance

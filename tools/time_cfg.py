@@ -10,7 +10,7 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 c = W.configs()[name]
 mode = fr.Mode[sys.argv[3]] if len(sys.argv) > 3 else (
     fr.Mode.FP32_FAST if c.precision == 32 else fr.Mode.FP64_FAST)
-pal = W.palette("classic") if c.colorize else None
+pal = W.palette("classic") if c.colorize and not os.environ.get("NOCOLOR") else None
 out = torch.empty((c.height, c.width), dtype=torch.uint16, device="cuda")
 rgba = torch.empty((c.height, c.width, 4), dtype=torch.uint8, device="cuda") if pal else None
 
