@@ -977,27 +977,10 @@ struct Workspace {
 };
 
 // Continuation of an in-flight pixel (kernel R's end-of-supply hand-off, see below).
-template <class T>
-struct ContEntry {
-  T x, y, cr, ci;  // state Z_cnt and C
-  int cnt;         // leading iterations already tested (exact count so far)
-  int pad;
-  int64_t off;     // output offset; < 0: empty slot
-};
-
-// How kernel R sources and ends its work.
-enum RefillMode {
-  kDrain = 0,     // chunks; at the end every warp drains its last pixels
-  kHandOff = 1,   // chunks; when the supply runs out the warp writes its in-flight
-                  //   pixels to its 32 ContEntry slots and exits (no drain)
-  kContinue = 2,  // items are the ContEntry slots of a kHandOff launch (n_chunks = slots)
-};
-
 template <class T, bool STRICT, bool MANDEL, bool COLOR, bool AMORT, int K, int TH>
 __global__ void __launch_bounds__(kThreads)
 escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Workspace* ws,
-                     unsigned n_chunks, unsigned chunks_per_cta, ContEntry<T>* cont,
-                     int mode) {
+                     unsigned n_chunks, unsigned chunks_per_cta) {
   __shared__ uchar4 spal[COLOR ? 256 : 1];
   __shared__ T tre[kThreads / 32][kTileW];
   __shared__ T tim[kThreads / 32][kTileH];
@@ -1038,90 +1021,55 @@ escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
     while (need != 0u && !exhausted) {
       if (next_idx >= kChunk) {
         unsigned cid = 0;
-        const unsigned step = (mode == kContinue) ? 32u : 1u;  // kContinue: 32 slots a grab
         if (lane == 0) cid = chunks_per_cta ? c_lo + atomicAdd(&s_next, 1u)
-                                            : atomicAdd(&ws->next_chunk, step);
+                                            : atomicAdd(&ws->next_chunk, 1u);
         cid = __shfl_sync(kFull, cid, 0);
         if (cid >= c_hi) {
           exhausted = true;
           if (trace && lane == 0) trace[gw * 3 + 1] = global_ns();
           break;
         }
-        if (mode == kContinue) {
-          chunk_x0 = (int)cid;  // first slot of the grab
-          chunk_y0 = (int)min(c_hi - cid, 32u);
-          next_idx = kChunk - chunk_y0;  // chunk_y0 slots available
-        } else {
-          const int cty = (int)(cid / (unsigned)g.tiles_x);
-          chunk_x0 = ((int)cid - cty * g.tiles_x) * kTileW;
-          chunk_y0 = cty * kTileH;
-          __syncwarp();
-          tre[warp][lane] = to_state<T, STRICT>(pixel_re(g, min(chunk_x0 + lane, g.W - 1)));
-          if (lane < kTileH)
-            tim[warp][lane] = to_state<T, STRICT>(
-                pixel_im(g, global_row(g, min(chunk_y0 + lane, g.rows - 1))));
-          __syncwarp();
-          next_idx = 0;
-        }
+        const int cty = (int)(cid / (unsigned)g.tiles_x);
+        chunk_x0 = ((int)cid - cty * g.tiles_x) * kTileW;
+        chunk_y0 = cty * kTileH;
+        __syncwarp();
+        tre[warp][lane] = to_state<T, STRICT>(pixel_re(g, min(chunk_x0 + lane, g.W - 1)));
+        if (lane < kTileH)
+          tim[warp][lane] = to_state<T, STRICT>(
+              pixel_im(g, global_row(g, min(chunk_y0 + lane, g.rows - 1))));
+        __syncwarp();
+        next_idx = 0;
       }
       const int avail = kChunk - next_idx;
       const int rank = __popc(need & lt_mask);
       const bool mine = (need >> lane) & 1u;
       bool got = false;
       if (mine && rank < avail) {
-        if (mode == kContinue) {
-          const ContEntry<T> e = cont[chunk_x0 + (next_idx - (kChunk - chunk_y0)) + rank];
-          if (e.off >= 0) {
-            got = true;
-            off = e.off;
-            x = e.x;
-            y = e.y;
-            cr = e.cr;
-            ci = e.ci;
-            cnt = e.cnt;
-            alive = 1u;
+        const int idx = next_idx + rank;
+        const int lx = idx & (kTileW - 1);
+        const int lyy = idx >> 5;
+        const int px = chunk_x0 + lx;
+        const int row = chunk_y0 + lyy;
+        if (px < g.W && row < g.rows) {  // else: off-frame pixel of an edge chunk, skipped
+          got = true;
+          off = (int64_t)row * g.W + px;
+          const T a = tre[warp][lx], b = tim[warp][lyy];
+          if (MANDEL) {
+            x = T(0);
+            y = T(0);
+            cr = a;
+            ci = b;
+          } else {
+            x = a;
+            y = b;
           }
-        } else {
-          const int idx = next_idx + rank;
-          const int lx = idx & (kTileW - 1);
-          const int lyy = idx >> 5;
-          const int px = chunk_x0 + lx;
-          const int row = chunk_y0 + lyy;
-          if (px < g.W && row < g.rows) {  // else: off-frame pixel of an edge chunk, skipped
-            got = true;
-            off = (int64_t)row * g.W + px;
-            const T a = tre[warp][lx], b = tim[warp][lyy];
-            if (MANDEL) {
-              x = T(0);
-              y = T(0);
-              cr = a;
-              ci = b;
-            } else {
-              x = a;
-              y = b;
-            }
-            alive = 1u;
-            cnt = 0;
-          }
+          alive = 1u;
+          cnt = 0;
         }
       }
       const int nneed = __popc(need);
       next_idx += nneed < avail ? nneed : avail;
       need = __ballot_sync(kFull, mine && !got);
-    }
-    if (!AMORT && mode == kHandOff && exhausted) {
-      // supply exhausted: hand the warp's in-flight pixels to the continuation launch
-      // (every lane writes its slot; lanes without a pixel mark it empty) and stop
-      ContEntry<T> e;
-      e.x = x;
-      e.y = y;
-      e.cr = cr;
-      e.ci = ci;
-      e.cnt = cnt;
-      e.pad = 0;
-      e.off = off;
-      cont[((int64_t)blockIdx.x * (kThreads / 32) + warp) * 32 + lane] = e;
-      break;
     }
     const int n_held = __popc(__ballot_sync(kFull, off >= 0));
     if (n_held == 0) break;  // chunks exhausted and every pixel stored

@@ -292,10 +292,8 @@ cudaError_t workspace_for(cudaStream_t s, fr::Workspace** out) {
   return cudaSuccess;
 }
 
-// Continuation slots for kernel R's hand-off (fr::ContEntry), cached per (device, stream)
-// and grown on demand; created outside any graph capture like the workspace.
-std::map<std::pair<int, uintptr_t>, std::pair<void*, size_t>> g_cont;
-
+// Library-owned device buffers cached per (device, stream), grown on demand and created
+// outside any graph capture (like the workspace).
 cudaError_t buffer_for(std::map<std::pair<int, uintptr_t>, std::pair<void*, size_t>>& g_cont,
                        cudaStream_t s, size_t bytes, void** out) {
   int dev = 0;
@@ -320,17 +318,6 @@ cudaError_t buffer_for(std::map<std::pair<int, uintptr_t>, std::pair<void*, size
   g_cont[key] = std::make_pair(p, bytes);
   *out = p;
   return cudaSuccess;
-}
-
-cudaError_t cont_buffer_for(cudaStream_t s, size_t bytes, void** out) {
-  return buffer_for(g_cont, s, bytes, out);
-}
-
-// Hand-off + continuation launch for kernel R (opt-in, FRACTAL_CONT=1): measured within
-// run-to-run noise of the single-launch drain on cfg3 (0.28-0.30 ms either way).
-bool cont_enabled() {
-  static const bool v = env_is("FRACTAL_CONT", "1");
-  return v;
 }
 
 int sm_count() {
@@ -363,8 +350,7 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
   cudaError_t e;
   if (cpc > 0) {
     const unsigned blocks = (n_chunks + cpc - 1) / cpc;
-    kern<<<blocks, fr::kThreads, 0, s>>>(g, pal, jcr, jci, nullptr, n_chunks, (unsigned)cpc,
-                                         nullptr, fr::kDrain);
+    kern<<<blocks, fr::kThreads, 0, s>>>(g, pal, jcr, jci, nullptr, n_chunks, (unsigned)cpc);
   } else {
     fr::Workspace* ws = nullptr;
     e = workspace_for(s, &ws);
@@ -380,31 +366,7 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
     const int64_t need = (n_chunks + fr::kThreads / 32 - 1) / (fr::kThreads / 32);
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
-    if (!AMORT && cont_enabled()) {
-      // hand-off: launch 1 renders until the chunk supply runs out, then every warp
-      // writes its in-flight pixels to its slots and exits; launch 2 -- one CTA per SM,
-      // so the long remaining orbits get a large share of each SM's issue slots --
-      // finishes them with the same lane refill
-      const size_t slots = (size_t)blocks * fr::kThreads;
-      void* buf = nullptr;
-      e = cont_buffer_for(s, slots * sizeof(fr::ContEntry<T>), &buf);
-      if (e != cudaSuccess) return e;
-      auto* cont = static_cast<fr::ContEntry<T>*>(buf);
-      kern<<<(unsigned)blocks, fr::kThreads, 0, s>>>(g, pal, jcr, jci, ws, n_chunks, 0u, cont,
-                                                     fr::kHandOff);
-      e = cudaGetLastError();
-      if (e != cudaSuccess) return e;
-      g_launches.fetch_add(1, std::memory_order_relaxed);
-      // continuation CTAs per SM (FRACTAL_CONT_CTAS, default 2)
-      static const int c2_env = env_int("FRACTAL_CONT_CTAS", 2);
-      const int c2 = c2_env < 1 ? 1 : (c2_env > occ ? occ : c2_env);
-      const unsigned blocks2 = (unsigned)(sm_count() * c2);
-      kern<<<blocks2, fr::kThreads, 0, s>>>(g, pal, jcr, jci, ws, (unsigned)slots, 0u, cont,
-                                            fr::kContinue);
-    } else {
-      kern<<<(unsigned)blocks, fr::kThreads, 0, s>>>(g, pal, jcr, jci, ws, n_chunks, 0u,
-                                                     nullptr, fr::kDrain);
-    }
+    kern<<<(unsigned)blocks, fr::kThreads, 0, s>>>(g, pal, jcr, jci, ws, n_chunks, 0u);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();

@@ -21,7 +21,6 @@ SUBSET = ("test_strict_configs_full_frame or test_strict_fuzz or test_strict_rag
                                  {"FRACTAL_SCHED": "twophase", "FRACTAL_BUDGET": "48",
                                   "FRACTAL_P2_OCC": "1"},
                                  {"FRACTAL_SCHED": "refill", "FRACTAL_REFILL_CPC": "16"},
-                                 {"FRACTAL_SCHED": "refill", "FRACTAL_CONT": "1"},
                                  {"FRACTAL_SCHED": "amort", "FRACTAL_REFILL_CPC": "0"}])
 def test_parity_under_forced_scheduler(env):
     torch = pytest.importorskip("torch")
