@@ -866,9 +866,19 @@ escape_cont_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Co
   if (trace && lane == 0) trace[gw * 3] = global_ns();
   bool exhausted = false;
   unsigned need = kFull;
-  unsigned gpos = 32u, gend = 0u;  // current grab [gpos, gend) of item positions
-  unsigned pf = 0u;                // lane 0: prefetched grab base
-  bool have_pf = false;
+  // Items are staged in registers, one per lane: `cur` holds the current grab of 32
+  // positions [cbase, cbase + 32), `nxt` the next one.  The next grab's atomic is issued
+  // when a grab becomes current and its items are loaded at the following dispense
+  // event, so a refill takes its item by shuffle with no memory latency.
+  unsigned cbase = 0u, gpos = 0u, gend = 0u;  // current grab; [gpos, gend) undispensed
+  QItem<T> cur{}, nxt{};
+  unsigned nbase = 0u;
+  bool nxt_loaded = false;  // nxt holds the items of grab nbase
+  unsigned pf = 0u;         // lane 0: base of the prefetched grab (valid if pf_issued)
+  bool pf_issued = false;
+  auto load_grab = [&](unsigned base, QItem<T>& dst) {
+    if (base + (unsigned)lane < n_items) dst = items[base + (unsigned)lane];
+  };
 
   T x = T(0), y = T(0), cr = jcr, ci = jci;
   unsigned alive = 0u;
@@ -878,35 +888,54 @@ escape_cont_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Co
   for (;;) {
     while (need != 0u && !exhausted) {
       if (gpos >= gend) {
-        unsigned base = 0u;
-        if (lane == 0) base = have_pf ? pf : atomicAdd(&q->head, 32u);
-        base = __shfl_sync(kFull, base, 0);
-        have_pf = false;
-        if (base >= n_items) {
+        // switch to the next grab: staged if possible, else fetch it now
+        if (!nxt_loaded) {
+          unsigned base = 0u;
+          if (lane == 0) base = pf_issued ? pf : atomicAdd(&q->head, 32u);
+          nbase = __shfl_sync(kFull, base, 0);
+          pf_issued = false;
+          if (nbase < n_items) load_grab(nbase, nxt);
+        }
+        nxt_loaded = false;
+        if (nbase >= n_items) {
           exhausted = true;
           if (trace && lane == 0) trace[gw * 3 + 1] = global_ns();
           break;
         }
-        gpos = base;
-        gend = min(base + 32u, n_items);
-        if (lane == 0 && gend < n_items) pf = atomicAdd(&q->head, 32u);
-        have_pf = gend < n_items;
+        cur = nxt;
+        cbase = nbase;
+        gpos = nbase;
+        gend = min(nbase + 32u, n_items);
+        if (gend < n_items) {  // prefetch the following grab
+          if (lane == 0) pf = atomicAdd(&q->head, 32u);
+          pf_issued = true;
+        }
+      } else if (pf_issued && !nxt_loaded) {
+        // the prefetch atomic has had a block to return: stage its items
+        nbase = __shfl_sync(kFull, pf, 0);
+        pf_issued = false;
+        nxt_loaded = true;
+        if (nbase < n_items) load_grab(nbase, nxt);
       }
       const unsigned avail = gend - gpos;
       const unsigned rank = (unsigned)__popc(need & lt_mask);
       const bool mine = (need >> lane) & 1u;
+      const int src = (int)(gpos - cbase + (rank < avail ? rank : 0u));
+      const T ix = __shfl_sync(kFull, cur.x, src);
+      const T iy = __shfl_sync(kFull, cur.y, src);
+      const int icnt = __shfl_sync(kFull, cur.cnt, src);
+      const unsigned iidx = __shfl_sync(kFull, cur.idx, src);
       bool got = false;
       if (mine && rank < avail) {
-        const QItem<T> it = items[gpos + rank];
         got = true;
-        off = it.idx;
-        x = it.x;
-        y = it.y;
-        cnt = it.cnt;
+        off = iidx;
+        x = ix;
+        y = iy;
+        cnt = icnt;
         alive = 1u;
         if (MANDEL) {
-          const int row = (int)(it.idx / (unsigned)g.W);
-          const int px = (int)(it.idx - (unsigned)row * (unsigned)g.W);
+          const int row = (int)(iidx / (unsigned)g.W);
+          const int px = (int)(iidx - (unsigned)row * (unsigned)g.W);
           cr = to_state<T, STRICT>(pixel_re(g, px));
           ci = to_state<T, STRICT>(pixel_im(g, global_row(g, row)));
         }
