@@ -31,3 +31,40 @@ def test_parity_under_forced_scheduler(env):
                         "-m", "gpu", "-q", "-x", "-k", SUBSET, "-p", "no:cacheprovider"],
                        cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+_HASH_SCRIPT = r"""
+import hashlib, sys
+import torch
+from paper_1611_03079_b200 import binding as fr
+from paper_1611_03079_b200 import workloads as W
+out = []
+for mode in ("FP32_FAST", "FP64_FAST", "FP32_STRICT"):
+    c3 = W.configs()["cfg3"]
+    win = W.julia_window(960, 540)
+    a = fr.julia_render_ex(c3.c, win, 960, 540, 1000, fr.Mode[mode])
+    m = fr.mandelbrot_param_map(W.mandel_window(640, 360), 640, 360, 700, fr.Mode[mode])
+    torch.cuda.synchronize()
+    for t in (a, m):
+        out.append(hashlib.sha256(t.view(torch.int16).cpu().numpy().tobytes()).hexdigest()[:16])
+print(" ".join(out))
+"""
+
+
+def test_fast_mode_identical_across_schedulers():
+    """FAST modes are one arithmetic (the contracted doubled-state step), whichever kernel
+    runs it: S/S2 (PTX vote loops), P1 + P2, R and A must give bit-identical counts for the
+    same frame, not merely counts within reading c-10."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    hashes = {}
+    for sched in ("static", "refill", "twophase", "amort"):
+        e = dict(os.environ, FRACTAL_SCHED=sched)
+        r = subprocess.run([sys.executable, "-c", _HASH_SCRIPT], cwd=ROOT, env=e,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        hashes[sched] = r.stdout.split()
+    ref = hashes["static"]
+    for sched, h in hashes.items():
+        assert h == ref, (sched, h, ref)
