@@ -326,6 +326,8 @@ def main():
     gather = measure_gather(out, world, rank, barrier) if world > 1 else None
     delivered = (measure_delivered(win, world, rank, barrier, job_iters / args.steps)
                  if world > 1 else None)
+    # ---- row bands over the ranks (cfg3 and cfg5 as cyclic bands)
+    bands = measure_bands(world, rank, barrier) if world > 1 and not args.no_extra else None
     # ---- end-to-end through the public API with HOST buffers (pinned), N GPUs
     e2e = measure_e2e(fr, W, cs, win, world, args, barrier, stream)
     if rank == 0:
@@ -334,6 +336,8 @@ def main():
             line["gather_to_rank0"] = gather
         if delivered is not None:
             line["delivered_to_rank0"] = delivered
+        if bands is not None:
+            line["bands"] = bands
         if world == 1:
             line["cpu_baseline"] = cpu_oracle_rate(cs, seconds=args.cpu_seconds)
             if not args.no_extra:
@@ -409,6 +413,68 @@ def measure_delivered(win, world, rank, barrier, job_iters_per_step, chunk=64):
                         "frames land in rank 0's buffer, path order is a zero-copy view"}
     except Exception as e:  # report, never fail the bench line
         return {"error": f"{type(e).__name__}: {e}"[:300]}
+
+
+def measure_bands(world, rank, barrier):
+    """cfg3 (4K Julia, mi 1000, fp32 fast) and cfg5 (16384^2 Mandelbrot, mi 10000, fp64
+    fast) as cyclic row bands over the ranks (band_rows 15 and 16): the compute makespan
+    (max over ranks of each rank's render) and the NCCL gather of the bands to rank 0
+    (distributed.gather_bands), timed separately with CUDA events."""
+    import torch
+    import torch.distributed as dist
+    from paper_1611_03079_b200 import binding as fr
+    from paper_1611_03079_b200 import distributed as D
+    from paper_1611_03079_b200 import workloads as W
+    out = {}
+    for name, reps in (("cfg3", 20), ("cfg5", 1)):
+        try:
+            c = W.configs()[name]
+            if c.kind == "julia":
+                mode = fr.Mode.FP32_FAST
+
+                def render():
+                    return D.render_bands("julia", c.window, c.width, c.height, c.max_iter,
+                                          c.band_rows, c=c.c, mode=mode, gather=False)
+            else:
+                mode = fr.Mode.FP64_FAST
+
+                def render():
+                    return D.render_bands("mandelbrot", c.window, c.width, c.height,
+                                          c.max_iter, c.band_rows, mode=mode, gather=False)
+            local = render()  # warm-up (workspaces, survivor buffer, NCCL set-up)
+            _ = D.gather_bands(local, c.height, c.band_rows)
+            del _
+            barrier()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record()
+            for _ in range(reps):
+                local = render()
+            t1.record()
+            barrier()
+            ms = t0.elapsed_time(t1) / reps
+            iters = float((local.view(torch.int16).to(torch.int64) & 0xFFFF).sum().item())
+            g0 = torch.cuda.Event(enable_timing=True)
+            g1 = torch.cuda.Event(enable_timing=True)
+            g0.record()
+            full = D.gather_bands(local, c.height, c.band_rows)
+            g1.record()
+            barrier()
+            gms = g0.elapsed_time(g1)
+            t = torch.tensor([ms, gms, iters], dtype=torch.float64, device="cuda")
+            mx = t.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            sm = t.clone()
+            dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+            del full, local
+            out[name] = {"compute_ms": float(mx[0]), "gather_ms": float(mx[1]),
+                         "gpix_iter_s": float(sm[2]) / (float(mx[0]) * 1e-3) / 1e9,
+                         "band_rows": c.band_rows, "mode": mode.name,
+                         "note": "cyclic bands, compute makespan = max over ranks; gather "
+                                 "of the uint16 bands to rank 0 (NCCL) timed separately"}
+        except Exception as e:  # report, never fail the bench line
+            out[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    return out
 
 
 def measure_e2e(fr, W, cs, win, world, args, barrier, stream):
