@@ -50,9 +50,25 @@ def fast(prec, fr):
     return fr.Mode.FP32_FAST if prec == 32 else fr.Mode.FP64_FAST
 
 
+def _sentinel_outputs(fr, w, h, mi, bands, palette):
+    """Output buffers pre-filled with a value no correct render leaves (count mi + 1;
+    RGBA 0x5A bytes), so a pixel a kernel never writes fails the comparison instead of
+    passing on stale memory from the caching allocator (a dropped-work bug once hid
+    behind exactly that)."""
+    rows = h if bands is fr.FULL_FRAME else fr.band_local_rows(h, bands)
+    s = (mi + 1) & 0xFFFF
+    out = torch.full((rows, w), s - 65536 if s >= 32768 else s, dtype=torch.int16,
+                     device="cuda").view(torch.uint16)
+    rgba = (torch.full((rows, w, 4), 0x5A, dtype=torch.uint8, device="cuda")
+            if palette is not None else None)
+    return out, rgba
+
+
 def gpu_julia(fr, c, win, w, h, mi, mode, bands=None, palette=None):
     bands = bands or fr.FULL_FRAME
-    r = fr.julia_render_ex(c, win, w, h, mi, mode, bands, palette=palette)
+    out, rgba = _sentinel_outputs(fr, w, h, mi, bands, palette)
+    r = fr.julia_render_ex(c, win, w, h, mi, mode, bands, out=out, palette=palette,
+                           out_rgba=rgba)
     torch.cuda.synchronize()
     if palette is not None:
         return np16(r[0]), r[1].cpu().numpy()
@@ -60,7 +76,9 @@ def gpu_julia(fr, c, win, w, h, mi, mode, bands=None, palette=None):
 
 
 def gpu_mandel(fr, win, w, h, mi, mode, bands=None):
-    r = fr.mandelbrot_param_map(win, w, h, mi, mode, bands or fr.FULL_FRAME)
+    bands = bands or fr.FULL_FRAME
+    out, _ = _sentinel_outputs(fr, w, h, mi, bands, None)
+    r = fr.mandelbrot_param_map(win, w, h, mi, mode, bands, out=out)
     torch.cuda.synchronize()
     return np16(r)
 
@@ -206,7 +224,11 @@ def test_path_equals_single_frames(fr):
     for mode, mi in ((fr.Mode.FP32_FAST, 100), (fr.Mode.FP32_FAST, 99),
                      (fr.Mode.FP32_STRICT, 100), (fr.Mode.FP64_FAST, 100)):
         pal = W.palette("fire")
-        frames, rgba = fr.julia_render_path(cs, win, w, h, mi, mode, palette=pal)
+        frames = torch.full((len(cs), h, w), mi + 1, dtype=torch.int16,
+                            device="cuda").view(torch.uint16)  # sentinel: never a count
+        rgba = torch.full((len(cs), h, w, 4), 0x5A, dtype=torch.uint8, device="cuda")
+        frames, rgba = fr.julia_render_path(cs, win, w, h, mi, mode, out=frames, palette=pal,
+                                            out_rgba=rgba)
         torch.cuda.synchronize()
         frames = np16(frames)
         rgba = rgba.cpu().numpy()
