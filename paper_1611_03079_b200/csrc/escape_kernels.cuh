@@ -947,7 +947,25 @@ escape_cont_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Co
     const int n_held = __popc(__ballot_sync(kFull, off >= 0));
     if (n_held == 0) break;
     const bool held = off >= 0;
-    const int thr = exhausted ? 1 : (TH < n_held ? TH : n_held);
+    if (exhausted) {
+      // Queue dry: nothing left to refill, so no per-lane servicing -- run blocks until
+      // no held orbit is still alive below max_iter (one vote per block), then store all.
+      // A finished lane's count is frozen (sticky alive), and iterating past max_iter
+      // is harmless (counts are clamped at the store).
+      if (!held) alive = 0u;
+      while (__any_sync(kFull, held && alive && cnt < max_iter)) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) It::step(x, y, cr, ci, alive, cnt);
+      }
+      if (held) {
+        const int count = cnt < max_iter ? cnt : max_iter;
+        g.counts[off] = (uint16_t)count;
+        if (COLOR) g.rgba[off] = colour_of(spal, pal, count, max_iter);
+        off = -1;
+      }
+      break;
+    }
+    const int thr = TH < n_held ? TH : n_held;
     const int lim = held ? max_iter : 0x7fffffff;
     if (!held) alive = 0u;
     bool fin;
