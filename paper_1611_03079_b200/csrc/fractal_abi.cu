@@ -422,10 +422,11 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
       o = 1;
     return o;
   }();
-  // P2 runs 3 CTAs per SM (FRACTAL_P2_OCC), not the occupancy limit: ~3 warps per SMSP
-  // already saturate issue for this loop, and every extra resident lane only adds to the
-  // work still in flight when the queue runs dry (cfg3: 8 CTAs 0.273 ms, 3 CTAs 0.228)
-  static const int occ_env = env_int("FRACTAL_P2_OCC", 3);
+  // P2 runs 2 CTAs per SM (FRACTAL_P2_OCC), not the occupancy limit: a few warps per
+  // SMSP already saturate issue for this loop, and every extra resident lane only adds
+  // to the work still in flight when the queue runs dry (cfg3: 8 CTAs 0.273 ms, 3 CTAs
+  // 0.1975, 2 CTAs 0.1965; strict 0.250 vs 0.246)
+  static const int occ_env = env_int("FRACTAL_P2_OCC", 2);
   const int occ2 = occ_env > 0 && occ_env < occ ? occ_env : occ;
   kern<<<(unsigned)(sm_count() * occ2), fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items);
   g_launches.fetch_add(1, std::memory_order_relaxed);
