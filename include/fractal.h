@@ -32,11 +32,22 @@
  *  Memory.  Every pointer named *_dev / out_* is DEVICE memory owned by the caller;
  *           the library keeps no pointer after return.  c_host and the palette are
  *           HOST memory, consumed (copied into kernel parameters) before return.
+ *           The library owns, per (device, stream), small scheduling workspaces
+ *           (chunk counters, a 384-B queue header), the survivor buffer of the
+ *           heavy-tailed two-phase path (one 16-B item per pixel, 24 B in fp64,
+ *           grown on demand, frames up to 2^25 pixels) and, per device, a 1-KB
+ *           device copy of each distinct palette.  They are created
+ *           on first use and live until process exit; creation is synchronous and
+ *           is not allowed inside CUDA graph capture (cudaErrorStreamCaptureUnsupported
+ *           -> FR_ERR_CUDA), so make the first call of a kind on a stream outside
+ *           capture.
  *  Async.   Calls validate synchronously, enqueue on `stream` and return.  Outputs
  *           are valid once the caller synchronises the stream; device faults surface
  *           there.  On any error status nothing has been launched.  No C++ exception
- *           crosses the ABI.  Calls are reentrant and thread-safe; the library holds
- *           no mutable state except a monotonic launch counter (fr_launch_count).
+ *           crosses the ABI.  Calls are reentrant and thread-safe (the caches above
+ *           are mutex-guarded; calls on one stream share its workspaces in stream
+ *           order); apart from those caches the library holds only a monotonic
+ *           launch counter (fr_launch_count).
  *  Stream.  `stream` is a cudaStream_t (NULL = legacy default stream).
  */
 #ifndef FRACTAL_H_
