@@ -429,8 +429,15 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   static const int occ_env = env_int("FRACTAL_P2_OCC", 2);
   const int occ2 = occ_env > 0 && occ_env < occ ? occ_env : occ;
   kern<<<(unsigned)(sm_count() * occ2), fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    // P2 resets the queue header when it finishes; if it never ran, reset it here so
+    // the next call does not start from P1's stale tail
+    cudaMemsetAsync(qp, 0, sizeof(fr::ContQueue), s);
+    return e;
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 template <bool MANDEL, bool COLOR>
