@@ -57,6 +57,17 @@ def path_for(world: int, rank: int):
     return full[rank::world]
 
 
+def arm_config(world: int) -> dict:
+    """The workload both arms report (ours and --impl reference)."""
+    return {"workload": "cfg4 C-path sweep (BASELINE configs[3]), weak-scaled: "
+                        f"{FRAMES_PER_RANK} frames/GPU, F={FRAMES_PER_RANK}*N frames "
+                        "on |C|=0.7885, frame k -> rank k mod N",
+            "width": W_PX, "height": H_PX, "max_iter": MAX_ITER, "mode": "FP32_FAST",
+            "frames_per_step": FRAMES_PER_RANK * world, "parallelism": f"frames{world}",
+            "l2": f"output {FRAMES_PER_RANK * W_PX * H_PX * 2 / 1e9:.2f} GB per step per "
+                  "GPU (> 126 MB L2), no L2 reuse between steps"}
+
+
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
     """Samples SM clock and throttle reasons DURING the timed region via NVML (every
@@ -188,9 +199,9 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "cfg4 C-path, 1080p, max_iter 100 (bounded sample)",
-                   "frames_per_step": per_step, "width": W_PX, "height": H_PX,
-                   "max_iter": MAX_ITER},
+        "config": arm_config(world),
+        "reference_sample": f"each step renders {per_step} random frames of the rank-0 batch "
+                            "of this workload (bounded sample); the rate is per pixel-iteration",
         "cpu_baseline": {"value": v, "unit": "Gpixel-iter/s", "cores": threads, "kind": "oracle",
                          "sample": f"{per_step} random frames of the rank-0 batch per step, "
                                    f"strict fp32 scalar C oracle on {threads} threads"},
@@ -308,13 +319,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": "cfg4 C-path sweep (BASELINE configs[3]), weak-scaled: "
-                                   f"{FRAMES_PER_RANK} frames/GPU, F={FRAMES_PER_RANK}*N frames "
-                                   "on |C|=0.7885, frame k -> rank k mod N",
-                       "width": W_PX, "height": H_PX, "max_iter": MAX_ITER, "mode": "FP32_FAST",
-                       "frames_per_step": nf * world, "parallelism": f"frames{world}",
-                       "l2": f"output {nf * W_PX * H_PX * 2 / 1e9:.2f} GB per step per GPU "
-                             "(> 126 MB L2), no L2 reuse between steps"},
+            "config": arm_config(world),
             "frames_per_s": frames_per_s,
             "pixel_iters_per_step": job_iters / args.steps,
             "gpu_launches": int(launches),
