@@ -468,10 +468,76 @@ __device__ __forceinline__ int fast_vote_loop2_f32<2>(float& x, float& y, int& c
       : "r"(kfull), "r"(0), "r"(0), "f"(cr2), "f"(ci2), "f"(cr2b), "f"(ci2b));
   return n;
 }
+// STRICT fp32, two orbits: the exact IEEE sequence of reading c-9 (every operation
+// separately rounded, no contraction -- explicit .rn), same operand layout and vote loop
+// as the fast version, so the sticky predicates stay predicates across blocks.
+#define FR_STRICT_STEP2                              \
+  "mul.rn.f32 xx, %0, %0;\n\t"                       \
+  "mul.rn.f32 xx2, %5, %5;\n\t"                      \
+  "mul.rn.f32 yy, %1, %1;\n\t"                       \
+  "mul.rn.f32 yy2, %6, %6;\n\t"                      \
+  "add.rn.f32 m, xx, yy;\n\t"                        \
+  "add.rn.f32 m2, xx2, yy2;\n\t"                     \
+  "setp.le.and.f32 pa, m, 0f40800000, pa;\n\t"       \
+  "setp.le.and.f32 pb, m2, 0f40800000, pb;\n\t"      \
+  "@pa add.s32 %2, %2, 1;\n\t"                       \
+  "@pb add.s32 %7, %7, 1;\n\t"                       \
+  "mul.rn.f32 xy, %0, %1;\n\t"                       \
+  "mul.rn.f32 xy2, %5, %6;\n\t"                      \
+  "sub.rn.f32 t, xx, yy;\n\t"                        \
+  "sub.rn.f32 t2, xx2, yy2;\n\t"                     \
+  "add.rn.f32 s, xy, xy;\n\t"                        \
+  "add.rn.f32 s2, xy2, xy2;\n\t"                     \
+  "add.rn.f32 %0, t, %12;\n\t"                       \
+  "add.rn.f32 %5, t2, %14;\n\t"                      \
+  "add.rn.f32 %1, s, %13;\n\t"                       \
+  "add.rn.f32 %6, s2, %15;\n\t"
+
+__device__ __forceinline__ int strict_vote_loop2_f32(float& x, float& y, int& cnt,
+                                                     unsigned& alive, float& x2, float& y2,
+                                                     int& cnt2, unsigned& alive2, float cr,
+                                                     float ci, float crb, float cib, int kfull) {
+  int n;
+  asm volatile(
+      "{\n\t.reg .pred pa, pb, pm;\n\t"
+      ".reg .f32 xx, yy, m, xy, t, s, xx2, yy2, m2, xy2, t2, s2;\n\t"
+      "setp.ne.u32 pa, %3, 0;\n\tsetp.ne.u32 pb, %8, 0;\n\tmov.u32 %4, 0;\n\t"
+      "setp.gt.s32 pm, %9, 0;\n\t@!pm bra FR_S4B_DONE;\n"
+      "FR_S4B_LOOP:\n\t" FR_STRICT_STEP2 FR_STRICT_STEP2 FR_STRICT_STEP2 FR_STRICT_STEP2
+      "add.s32 %4, %4, 4;\n\t"
+      "or.pred pm, pa, pb;\n\t"
+      "vote.sync.any.pred pm, pm, 0xffffffff;\n\t"
+      "setp.lt.and.s32 pm, %4, %9, pm;\n\t"
+      "@pm bra FR_S4B_LOOP;\n"
+      "FR_S4B_DONE:\n\t"
+      "selp.u32 %3, 1, 0, pa;\n\tselp.u32 %8, 1, 0, pb;\n\t}"
+      : "+f"(x), "+f"(y), "+r"(cnt), "+r"(alive), "=r"(n), "+f"(x2), "+f"(y2), "+r"(cnt2),
+        "+r"(alive2)
+      : "r"(kfull), "r"(0), "r"(0), "f"(cr), "f"(ci), "f"(crb), "f"(cib));
+  return n;
+}
+#undef FR_STRICT_STEP2
+
+// Two-orbit PTX vote loop of either fp32 mode (blocks of 4).
+template <bool STRICT>
+__device__ __forceinline__ int vote_loop2_f32(float& x, float& y, int& cnt, unsigned& alive,
+                                              float& x2, float& y2, int& cnt2, unsigned& alive2,
+                                              float cr, float ci, float crb, float cib,
+                                              int kfull) {
+  if constexpr (STRICT)
+    return strict_vote_loop2_f32(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, crb, cib, kfull);
+  else
+    return fast_vote_loop2_f32<4>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, crb, cib, kfull);
+}
+
 #undef FR_FAST_STEP2
 
 template <class T, bool STRICT, int K>
 constexpr bool kAsmLoop = std::is_same<T, float>::value && !STRICT && (K == 2 || K == 4);
+// two-orbit PTX loops: fp32, both modes (strict: the exact sequence), blocks of 4 (fast
+// also 2)
+template <class T, bool STRICT, int K>
+constexpr bool kAsmPair = std::is_same<T, float>::value && (K == 4 || (!STRICT && K == 2));
 
 // ----------------------------------------------------------------------------------
 // Static-tile kernel (S): one pixel per thread, 8x4 warp tiles in a 32x8 CTA tile.  The
@@ -550,7 +616,7 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
   };
 
   int f = f0;
-  if constexpr (FN == 0 && kAsmLoop<T, STRICT, K> && !MANDEL && NC > 1) {
+  if constexpr (FN == 0 && kAsmPair<T, STRICT, K> && !MANDEL && NC > 1) {
     // two frames per lane (ILP); the remaining odd frame goes through the loop below
     for (; f + 1 < f1; f += 2) {
       float x = are, y = aim, x2 = are, y2 = aim;
@@ -559,11 +625,19 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
       // C values through a shuffle: they then live in per-thread registers, so the FFMA
       // X' = T * 0.5 + CR2 keeps 0.5 as an immediate (a uniform-register C forces ptxas
       // to rematerialise 0.5 with an extra ALU move every iteration: +18% instructions)
-      int n = fast_vote_loop2_f32<K>(x, y, cnt, alive, x2, y2, cnt2, alive2,
-                                     __shfl_sync(kFull, cs.re[f], lane),
-                                     __shfl_sync(kFull, cs.im[f], lane),
-                                     __shfl_sync(kFull, cs.re[f + 1], lane),
-                                     __shfl_sync(kFull, cs.im[f + 1], lane), kfull);
+      int n;
+      if constexpr (STRICT)
+        n = strict_vote_loop2_f32(x, y, cnt, alive, x2, y2, cnt2, alive2,
+                                  __shfl_sync(kFull, cs.re[f], lane),
+                                  __shfl_sync(kFull, cs.im[f], lane),
+                                  __shfl_sync(kFull, cs.re[f + 1], lane),
+                                  __shfl_sync(kFull, cs.im[f + 1], lane), kfull);
+      else
+        n = fast_vote_loop2_f32<K>(x, y, cnt, alive, x2, y2, cnt2, alive2,
+                                   __shfl_sync(kFull, cs.re[f], lane),
+                                   __shfl_sync(kFull, cs.im[f], lane),
+                                   __shfl_sync(kFull, cs.re[f + 1], lane),
+                                   __shfl_sync(kFull, cs.im[f + 1], lane), kfull);
       if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
         for (; n < max_iter; ++n) {
           Iter<T, STRICT>::step(x, y, cs.re[f], cs.im[f], alive, cnt);
@@ -796,8 +870,8 @@ escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
   unsigned alive = in0 ? 1u : 0u, alive2 = in1 ? 1u : 0u;
   int cnt = 0, cnt2 = 0;
   // budget is a multiple of 4 and < max_iter (host)
-  if constexpr (kAsmLoop<T, STRICT, 4>) {
-    fast_vote_loop2_f32<4>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2, budget);
+  if constexpr (kAsmPair<T, STRICT, 4>) {
+    vote_loop2_f32<STRICT>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2, budget);
   } else {
     for (int n = 0; n < budget; n += 4) {
 #pragma unroll
