@@ -729,15 +729,16 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
 }
 
 // ----------------------------------------------------------------------------------
-// Static-tile kernel for ONE frame, fast fp32, two pixels per thread (S2): CTA tile
+// Static-tile kernel for ONE frame, fp32 (fast or strict), two pixels per thread (S2): CTA tile
 // 32x16, each thread iterates the pixels of rows ly and ly + 8 of its 8x4-lane warp
 // tile together in the two-orbit PTX vote loop (ILP for the FP pipe, one vote for
 // both, half the per-pixel overhead).  Julia frames share C; Mandelbrot maps take each
 // orbit's C from its pixel (Z_0 = 0).  Bit-identical to kernel S (same arithmetic).
 // ----------------------------------------------------------------------------------
-template <bool MANDEL, bool COLOR>
+template <bool STRICT, bool MANDEL, bool COLOR>
 __global__ void __launch_bounds__(kThreads)
 escape_tile2_kernel(const Geom g, const Palette pal, const float jcr2, const float jci2) {
+  // jcr2/jci2: the Julia C in the state representation (doubled in FAST, plain in STRICT)
   // colours from the device palette (no CTA barrier in these short-lived CTAs)
   int tx, ty, grp;
   tile_of(g, tx, ty, grp);
@@ -750,9 +751,9 @@ escape_tile2_kernel(const Geom g, const Palette pal, const float jcr2, const flo
   const int ly1 = ly0 + kTileH;
   const bool in0 = (px < g.W) && (ly0 < g.rows);
   const bool in1 = (px < g.W) && (ly1 < g.rows);
-  const float re = to_state<float, false>(pixel_re(g, min(px, g.W - 1)));
-  const float im0 = to_state<float, false>(pixel_im(g, global_row(g, min(ly0, g.rows - 1))));
-  const float im1 = to_state<float, false>(pixel_im(g, global_row(g, min(ly1, g.rows - 1))));
+  const float re = to_state<float, STRICT>(pixel_re(g, min(px, g.W - 1)));
+  const float im0 = to_state<float, STRICT>(pixel_im(g, global_row(g, min(ly0, g.rows - 1))));
+  const float im1 = to_state<float, STRICT>(pixel_im(g, global_row(g, min(ly1, g.rows - 1))));
   float x, y, x2, y2, cr, ci, cr2, ci2;
   if (MANDEL) {
     x = y = x2 = y2 = 0.0f;
@@ -772,11 +773,11 @@ escape_tile2_kernel(const Geom g, const Palette pal, const float jcr2, const flo
   int cnt = 0, cnt2 = 0;
   const int max_iter = g.max_iter;
   const int kfull = max_iter - max_iter % 4;
-  int n = fast_vote_loop2_f32<4>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2, kfull);
+  int n = vote_loop2_f32<STRICT>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2, kfull);
   if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
     for (; n < max_iter; ++n) {
-      Iter<float, false>::step(x, y, cr, ci, alive, cnt);
-      Iter<float, false>::step(x2, y2, cr2, ci2, alive2, cnt2);
+      Iter<float, STRICT>::step(x, y, cr, ci, alive, cnt);
+      Iter<float, STRICT>::step(x2, y2, cr2, ci2, alive2, cnt2);
     }
   }
   if (in0) {

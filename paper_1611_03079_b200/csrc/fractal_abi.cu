@@ -178,12 +178,12 @@ cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr:
   static const int fpc_env = env_int("FRACTAL_FPC", 0);
   const int fpc_want = fpc_env > 0 ? fpc_env : kFramesPerCta;
   const int fpc = n_frames < fpc_want ? n_frames : fpc_want;
-  // one frame, fast fp32: two pixels per thread (kernel S2; FRACTAL_S2=0 disables)
+  // one frame, fp32 (either mode): two pixels per thread (kernel S2; FRACTAL_S2=0 disables)
   static const bool s2 = !env_is("FRACTAL_S2", "0");
-  if constexpr (NC == 1 && std::is_same<T, float>::value && !STRICT) {
+  if constexpr (NC == 1 && std::is_same<T, float>::value) {
     if (s2 && g.counts8 == nullptr) {
       const dim3 grid2 = tile_grid(g, (g.rows + 2 * fr::kTileH - 1) / (2 * fr::kTileH), 1);
-      fr::escape_tile2_kernel<MANDEL, COLOR>
+      fr::escape_tile2_kernel<STRICT, MANDEL, COLOR>
           <<<grid2, fr::kThreads, 0, s>>>(g, pal, cs.re[0], cs.im[0]);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return cudaGetLastError();
