@@ -616,7 +616,38 @@ def extras(fr, W, torch):
         del out, rgba
     torch.cuda.empty_cache()
     res["colorize_hbm"] = colorize_bandwidth(fr, W, torch)
+    res["cardioid_path"] = cardioid_path_rate(fr, W, torch, f_max)
     return res
+
+
+def cardioid_path_rate(fr, W, torch, f_max):
+    """NEXT-2: the paper's own C-path -- 512 frames of 1080p along the a = 3.9
+    cardioid (fr_cardioid_path), max_iter 100, FP32_FAST, through julia_render_path."""
+    try:
+        cs = fr.cardioid_path(512)
+        win = W.julia_window(W_PX, H_PX)
+        out = torch.empty((len(cs), H_PX, W_PX), dtype=torch.uint16, device="cuda")
+        fr.julia_render_path(cs, win, W_PX, H_PX, MAX_ITER, fr.Mode.FP32_FAST, out=out)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        reps = 3
+        a.record()
+        for _ in range(reps):
+            fr.julia_render_path(cs, win, W_PX, H_PX, MAX_ITER, fr.Mode.FP32_FAST, out=out)
+        b.record()
+        b.synchronize()
+        ms = a.elapsed_time(b) / reps
+        s = float((out.view(torch.int16).to(torch.int64) & 0xFFFF).sum().item())
+        peak = SM_COUNT * FP32_LANES_PER_SM * f_max * 1e6 / ALG_OPS_PER_ITER / 1e9
+        del out
+        return {"frames": len(cs), "ms": ms, "frames_per_s": len(cs) / (ms * 1e-3),
+                "gpix_iter_s": s / (ms * 1e-3) / 1e9,
+                "mean_iters_per_px": s / (len(cs) * W_PX * H_PX),
+                "frac_of_alu_peak": s / (ms * 1e-3) / 1e9 / peak,
+                "note": "cardioid a = 3.9, clockwise (fr_cardioid_path), kernel S"}
+    except Exception as e:  # report, never fail the line
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
 
 
 def colorize_bandwidth(fr, W, torch):
