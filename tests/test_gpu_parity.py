@@ -589,3 +589,35 @@ def test_path_to_host_buffers(fr):
     page16 = np.empty((70, h, w), dtype=np.uint16)
     fr.julia_render_path_host(cs, win, w, h, 100, fr.Mode.FP32_FAST, out=page16)
     np.testing.assert_array_equal(page16, ref)
+
+
+def test_graph_capture_contract(fr):
+    """fractal.h 'Memory': library caches are created outside graph capture.  A palette
+    first seen inside a capture fails cleanly (FractalError, nothing launched); once used
+    outside capture, the same coloured render captures and replays, and the replay equals
+    an eager render."""
+    cfg = W.configs()["cfg2"]
+    w, h = 320, 180
+    win = W.julia_window(w, h)
+    fresh = (np.arange(4 * 7, dtype=np.uint8).reshape(7, 4) * 9 + 3, (1, 2, 3, 255))
+    out = torch.empty((h, w), dtype=torch.uint16, device="cuda")
+    rgba = torch.empty((h, w, 4), dtype=torch.uint8, device="cuda")
+    side = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(fr.FractalError):
+        with torch.cuda.graph(g, stream=side):
+            fr.julia_render_ex(cfg.c, win, w, h, 100, fr.Mode.FP32_FAST, out=out,
+                               palette=fresh, out_rgba=rgba)
+    torch.cuda.synchronize()
+    # eager first use creates the device copy; then capture works
+    want_c, want_rgba = gpu_julia(fr, cfg.c, win, w, h, 100, fr.Mode.FP32_FAST, palette=fresh)
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2, stream=side):
+        fr.julia_render_ex(cfg.c, win, w, h, 100, fr.Mode.FP32_FAST, out=out, palette=fresh,
+                           out_rgba=rgba)
+    out.zero_()
+    rgba.zero_()
+    g2.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(np16(out), want_c)
+    np.testing.assert_array_equal(rgba.cpu().numpy(), want_rgba)
