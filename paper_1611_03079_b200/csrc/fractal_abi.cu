@@ -155,12 +155,9 @@ fr::Geom make_geom(fr_window win, int32_t width, int32_t height, int32_t max_ite
   return g;
 }
 
-// iterations per vote block of the static kernel (FRACTAL_STATIC_K=2|4 for fp32 fast)
+// iterations per vote block of the static kernel (fp64: 8).  K = 2 for fp32 fast was
+// measured slower on the bench workload (3.46 vs 3.44 ms).
 constexpr int kStaticK = 4;
-int static_k() {
-  static const int k = env_is("FRACTAL_STATIC_K", "2") ? 2 : 4;
-  return k;
-}
 constexpr int kFramesPerCta = 32;  // frames of a path chunk rendered per CTA (static kernel); FRACTAL_FPC overrides
 
 // Launch grid of kernels S/S2: (tiles_x, tiles_y, groups) when tiles_y fits grid y
@@ -197,9 +194,6 @@ cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr:
           <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);
     else
       return cudaErrorInvalidValue;
-  } else if (sizeof(T) == 4 && !STRICT && static_k() == 2) {
-    fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, 2, NC>
-        <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);
   } else {
     fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, KD, NC>
         <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);
@@ -454,72 +448,25 @@ cudaError_t launch_twophase_mode(fr_mode mode, const fr::Geom& g, const fr::Pale
   return cudaErrorInvalidValue;
 }
 
-// Tuning variants of the refill kernel for FP32_FAST (FRACTAL_REFILL=K,TH); default 16,8.
-int refill_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("FRACTAL_REFILL");
-    int v = 0;
-    if (e) {
-      if (!std::strcmp(e, "8,8")) v = 1;
-      else if (!std::strcmp(e, "16,16")) v = 2;
-      else if (!std::strcmp(e, "16,24")) v = 3;
-      else if (!std::strcmp(e, "32,16")) v = 4;
-      else if (!std::strcmp(e, "8,16")) v = 5;
-      else if (!std::strcmp(e, "16,1")) v = 6;
-      else if (!std::strcmp(e, "16,4")) v = 7;
-    }
-    return v;
-  }();
-  return v;
-}
-
+// Kernel R: blocks of 16, service threshold 8 (cfg3 sweep: K 8-32 and
+// TH 1-24 all within 0.30-0.36 ms, 16,8 best).
 template <bool MANDEL, bool COLOR>
 cudaError_t launch_refill_mode(fr_mode mode, const fr::Geom& g, const fr::Palette& pal,
                                double2 c, cudaStream_t s) {
   switch (mode) {
-    case FR_FP32_FAST:
-      switch (refill_variant()) {
-        case 1: return launch_refill_t<float, false, MANDEL, COLOR, 8, 8>(g, pal, c, s);
-        case 2: return launch_refill_t<float, false, MANDEL, COLOR, 16, 16>(g, pal, c, s);
-        case 3: return launch_refill_t<float, false, MANDEL, COLOR, 16, 24>(g, pal, c, s);
-        case 4: return launch_refill_t<float, false, MANDEL, COLOR, 32, 16>(g, pal, c, s);
-        case 5: return launch_refill_t<float, false, MANDEL, COLOR, 8, 16>(g, pal, c, s);
-        case 6: return launch_refill_t<float, false, MANDEL, COLOR, 16, 1>(g, pal, c, s);
-        case 7: return launch_refill_t<float, false, MANDEL, COLOR, 16, 4>(g, pal, c, s);
-        default: return launch_refill_t<float, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
-      }
-    case FR_FP32_STRICT:
-      return launch_refill_t<float, true, MANDEL, COLOR, 16, 8>(g, pal, c, s);
-    case FR_FP64_FAST:
-      return launch_refill_t<double, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
-    case FR_FP64_STRICT:
-      return launch_refill_t<double, true, MANDEL, COLOR, 16, 8>(g, pal, c, s);
+    case FR_FP32_FAST: return launch_refill_t<float, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
+    case FR_FP32_STRICT: return launch_refill_t<float, true, MANDEL, COLOR, 16, 8>(g, pal, c, s);
+    case FR_FP64_FAST: return launch_refill_t<double, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
+    case FR_FP64_STRICT: return launch_refill_t<double, true, MANDEL, COLOR, 16, 8>(g, pal, c, s);
   }
   return cudaErrorInvalidValue;
 }
 
-// Kernel A variants (FRACTAL_AMORT=K,TH).  Default 64,4: measured on cfg5 (fp64 fast)
-// 592 ms; 32,4 609; 128,4 597; 64,8 601; 16,1 641-663.
-int amort_variant() {
-  static const int v = env_is("FRACTAL_AMORT", "16,1") ? 0 : env_is("FRACTAL_AMORT", "16,4") ? 1
-                       : env_is("FRACTAL_AMORT", "16,8") ? 2 : env_is("FRACTAL_AMORT", "32,1") ? 3
-                       : env_is("FRACTAL_AMORT", "32,4") ? 4 : env_is("FRACTAL_AMORT", "128,4") ? 6
-                       : env_is("FRACTAL_AMORT", "64,8") ? 7 : 5;
-  return v;
-}
-
+// Kernel A: blocks of 64, service threshold 4 (cfg5 fp64 fast sweep, DESIGN.md §5.3:
+// 64,4 592 ms; 32,4 609; 128,4 597; 64,8 601; 16,1 641-663).
 template <class T, bool STRICT, bool MANDEL, bool COLOR>
 cudaError_t launch_amort_t(const fr::Geom& g, const fr::Palette& pal, double2 c, cudaStream_t s) {
-  switch (amort_variant()) {
-    case 1: return launch_refill_t<T, STRICT, MANDEL, COLOR, 16, 4, true>(g, pal, c, s);
-    case 2: return launch_refill_t<T, STRICT, MANDEL, COLOR, 16, 8, true>(g, pal, c, s);
-    case 3: return launch_refill_t<T, STRICT, MANDEL, COLOR, 32, 1, true>(g, pal, c, s);
-    case 4: return launch_refill_t<T, STRICT, MANDEL, COLOR, 32, 4, true>(g, pal, c, s);
-    case 6: return launch_refill_t<T, STRICT, MANDEL, COLOR, 128, 4, true>(g, pal, c, s);
-    case 7: return launch_refill_t<T, STRICT, MANDEL, COLOR, 64, 8, true>(g, pal, c, s);
-    case 0: return launch_refill_t<T, STRICT, MANDEL, COLOR, 16, 1, true>(g, pal, c, s);
-    default: return launch_refill_t<T, STRICT, MANDEL, COLOR, 64, 4, true>(g, pal, c, s);
-  }
+  return launch_refill_t<T, STRICT, MANDEL, COLOR, 64, 4, true>(g, pal, c, s);
 }
 
 template <bool MANDEL, bool COLOR>

@@ -37,9 +37,10 @@ def sass():
 
 
 def _fast_f32(name):
-    # escape_tile_kernel / escape_refill_kernel with T = float, STRICT = false; tile2
-    return (re.search(r"escape_(tile|refill)_kernelIfLb0E", name) is not None
-            or "escape_tile2_kernel" in name)
+    # escape_tile / escape_refill / escape_budget / escape_cont kernels with T = float,
+    # STRICT = false; escape_tile2_kernel<STRICT = false, ...>
+    return (re.search(r"escape_(tile|refill|budget|cont)_kernelIfLb0E", name) is not None
+            or "escape_tile2_kernelILb0E" in name)
 
 
 def test_sm100a(sass):
