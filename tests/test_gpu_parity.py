@@ -127,6 +127,20 @@ def test_strict_fuzz(fr, case):
         np.testing.assert_array_equal(gpu_mandel(fr, win, w, h, mi, strict(prec, fr)), ref)
 
 
+@pytest.mark.parametrize("case", range(32))
+def test_strict_fuzz_large(fr, case):
+    """A second seeded set with larger, ragged frames (up to 600 px a side) and
+    max_iter in {100, 300, 1000}: the two-phase path (P1 + P2) and S2 on many windows,
+    strict fp32 and fp64, Julia and Mandelbrot, bit-exact."""
+    c, win, w, h, _ = W.fuzz_cases(32, max_side=600, seed=W.FUZZ_SEED + 1)[case]
+    mi = (100, 300, 1000)[case % 3]
+    for prec in (32, 64):
+        ref = oracle.julia(c, win.center, win.half_w, win.half_h, w, h, mi, prec)
+        np.testing.assert_array_equal(gpu_julia(fr, c, win, w, h, mi, strict(prec, fr)), ref)
+        ref = oracle.mandelbrot(win.center, win.half_w, win.half_h, w, h, mi, prec)
+        np.testing.assert_array_equal(gpu_mandel(fr, win, w, h, mi, strict(prec, fr)), ref)
+
+
 @pytest.mark.parametrize("size", [(1, 1), (1, 37), (37, 1), (33, 9), (31, 7), (257, 129),
                                   (8, 4), (32, 8), (65, 17)])
 @pytest.mark.parametrize("mi", [1, 2, 7, 100])
