@@ -443,6 +443,29 @@ def test_fast_mode_tolerance_cfg4_frames(fr):
                           np16(out[i]), ref, f"cfg4 frame {k}")
 
 
+def test_bench_launch_fast_frames(fr):
+    """The exact launch bench.py times (512 frames of the |C| = 0.7885 circle path of
+    F = 512, 1080p, max_iter 100, FP32_FAST, one julia_render_path call): sampled frames
+    are byte-identical to independent single-frame renders (kernel S2; FAST is one
+    arithmetic across kernels) and within reading c-10 of the strict oracle."""
+    cfg = W.configs()["cfg4"]
+    cs = W.circle_path(512, 0.7885)
+    win = W.julia_window(1920, 1080)
+    out = torch.full((512, 1080, 1920), 101, dtype=torch.int16, device="cuda").view(torch.uint16)
+    fr.julia_render_path(cs, win, 1920, 1080, 100, fr.Mode.FP32_FAST, out=out)
+    torch.cuda.synchronize()
+    assert not bool((out.view(torch.int16) == 101).any()), "unwritten pixels"
+    for k in (0, 1, 127, 256, 383, 511):
+        one = gpu_julia(fr, complex(cs[k]), win, 1920, 1080, 100, fr.Mode.FP32_FAST)
+        np.testing.assert_array_equal(np16(out[k]), one)
+        ref = oracle.julia(complex(cs[k]), win.center, win.half_w, win.half_h, 1920, 1080,
+                           100, 32)
+        _check_fast_frame("julia", complex(cs[k]), win, 1920, 1080, 100, 32, one, ref,
+                          f"bench frame {k}")
+    del out
+    torch.cuda.empty_cache()
+
+
 def test_fast_mode_tolerance_cfg5_sampled(fr):
     cfg = W.configs()["cfg5"]
     win = cfg.window
