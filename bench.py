@@ -518,13 +518,15 @@ def measure_e2e(fr, W, cs, win, world, args, barrier, stream):
     dev = torch.empty((nf, H_PX, W_PX), dtype=torch.uint8, device="cuda")
     host.copy_(dev, non_blocking=True)
     torch.cuda.synchronize()
-    c0 = torch.cuda.Event(enable_timing=True)
-    c1 = torch.cuda.Event(enable_timing=True)
-    c0.record()
-    host.copy_(dev, non_blocking=True)
-    c1.record()
-    torch.cuda.synchronize()
-    copy_gbs = dev.numel() / (c0.elapsed_time(c1) * 1e-3) / 1e9
+    copy_gbs = 0.0
+    for _ in range(3):  # best of three: PCIe rates vary from copy to copy
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        c0.record()
+        host.copy_(dev, non_blocking=True)
+        c1.record()
+        torch.cuda.synchronize()
+        copy_gbs = max(copy_gbs, dev.numel() / (c0.elapsed_time(c1) * 1e-3) / 1e9)
     del dev
     tot = torch.tensor([float(iters)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -534,8 +536,8 @@ def measure_e2e(fr, W, cs, win, world, args, barrier, stream):
             "steps": steps, "ms_per_step": ms / steps,
             "d2h_GB_per_s": nf * H_PX * W_PX / (ms / steps * 1e-3) / 1e9,
             "d2h_copy_peak_GB_per_s": copy_gbs,
-            "bound": "PCIe device->host: d2h_copy_peak_GB_per_s is one plain pinned copy of "
-                     "the same bytes (torch), measured in this run",
+            "bound": "PCIe device->host: d2h_copy_peak_GB_per_s is the best of three plain "
+                     "pinned copies of the same bytes (torch), measured in this run",
             "api": "julia_render_path_host (C ABI, host output buffer)",
             "note": "C values (16 B/frame) host->device as kernel parameters; uint8 counts "
                     "device->host into pinned memory inside the call, 128 MiB chunks "

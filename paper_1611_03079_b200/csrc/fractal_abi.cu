@@ -726,9 +726,13 @@ fr_status julia_render_path_host(const fr_complex* c_host, int32_t n_frames, fr_
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
   }
   fr_status rs = FR_OK;
-  for (int32_t f0 = 0, i = 0; f0 < n_frames && e == cudaSuccess && rs == FR_OK; f0 += chunk, ++i) {
+  // the first chunk's render is the only one not hidden behind a copy: keep it small
+  const int32_t first = chunk / 8 > 0 ? chunk / 8 : 1;
+  for (int32_t f0 = 0, i = 0, nf = 0; f0 < n_frames && e == cudaSuccess && rs == FR_OK;
+       f0 += nf, ++i) {
     const int b = i & 1;
-    const int32_t nf = n_frames - f0 < chunk ? n_frames - f0 : chunk;
+    const int32_t want = i == 0 ? first : chunk;
+    nf = n_frames - f0 < want ? n_frames - f0 : want;
     if (i >= 2) e = cudaStreamWaitEvent(s, copied[b], 0);  // buffer b's copy is done
     if (e != cudaSuccess) break;
     rs = bytes_per_count == 2
