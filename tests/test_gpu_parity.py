@@ -577,24 +577,31 @@ def test_outputs_written_exactly_in_bounds(fr, size):
     w, h = size
     win = W.julia_window(w, h)
     pal = W.palette("fire")
-    for mi in (50, 300, 1200):  # static / refill / amortised (Mandelbrot) dispatch
-        for kind in ("julia", "mandelbrot"):
-            for bands in (fr.FULL_FRAME, fr.Bands(4, 3, 1)):
-                rows = fr.band_local_rows(h, bands)
-                fc, vc = _guarded(rows * w, torch.int16)
-                fr_, vr = _guarded(rows * w * 4, torch.uint8)
-                cnt = vc.view(torch.uint16)
-                if kind == "julia":
-                    fr.julia_render_ex(0.285 + 0.01j, win, w, h, mi, fr.Mode.FP32_FAST, bands,
-                                       out=cnt, palette=pal, out_rgba=vr)
-                else:
-                    fr.mandelbrot_param_map((-0.5 + 0j, 1.5, 1.5 * h / w), w, h, mi,
-                                            fr.Mode.FP64_FAST, bands, out=cnt, palette=pal,
-                                            out_rgba=vr)
-                torch.cuda.synchronize()
-                body = _check_canaries(fc, rows * w, torch.int16)
-                assert (body != -1).all()
-                _check_canaries(fr_, rows * w * 4, torch.uint8)
+    # max_iter 50: S2 (fp32) / S (fp64); 300 and 1200: P1 + P2; the monotone Mandelbrot
+    # window at 1200: kernel A; fast and strict modes
+    cases = [(mi, kind, strict_m) for mi in (50, 300, 1200) for kind in ("julia", "mandelbrot")
+             for strict_m in (False, True)] + [(1200, "mandel_mono", False),
+                                               (1200, "mandel_mono", True)]
+    for mi, kind, strict_m in cases:
+        for bands in (fr.FULL_FRAME, fr.Bands(4, 3, 1)):
+            rows = fr.band_local_rows(h, bands)
+            fc, vc = _guarded(rows * w, torch.int16)
+            fr_, vr = _guarded(rows * w * 4, torch.uint8)
+            cnt = vc.view(torch.uint16)
+            if kind == "julia":
+                m = fr.Mode.FP32_STRICT if strict_m else fr.Mode.FP32_FAST
+                fr.julia_render_ex(0.285 + 0.01j, win, w, h, mi, m, bands,
+                                   out=cnt, palette=pal, out_rgba=vr)
+            else:
+                m = fr.Mode.FP64_STRICT if strict_m else fr.Mode.FP64_FAST
+                mw = ((-0.5 + 0j, 1.5, 1.5 * h / w) if kind == "mandelbrot"
+                      else (-0.3 + 0.1j, 0.4, 0.4 * h / w))  # |C| <= 1.989: kernel A
+                fr.mandelbrot_param_map(mw, w, h, mi, m, bands, out=cnt, palette=pal,
+                                        out_rgba=vr)
+            torch.cuda.synchronize()
+            body = _check_canaries(fc, rows * w, torch.int16)
+            assert (body != -1).all()
+            _check_canaries(fr_, rows * w * 4, torch.uint8)
     n = 3
     fc, vc = _guarded(n * h * w, torch.int16)
     fr.julia_render_path(W.circle_path(n), win, w, h, 100, fr.Mode.FP32_FAST, out=vc.view(torch.uint16))
