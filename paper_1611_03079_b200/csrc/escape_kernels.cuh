@@ -2,6 +2,19 @@
 //
 // Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, "reading c-k" = DESIGN.md
 // §Readings.  Nothing here is shared with oracle/ (which is plain C, test-only).
+//
+// Kernels (DESIGN.md §5 has the dispatch table and the measurements):
+//   escape_tile_kernel    S   static tiles; frame groups of a C-path, two frames per lane
+//   escape_tile2_kernel   S2  one fp32 frame, two pixels per thread
+//   escape_budget_kernel  P1  heavy-tailed frames: static pass up to a budget, survivors
+//                             appended to a queue
+//   escape_cont_kernel    P2  persistent lane refill over P1's survivors
+//   escape_refill_kernel  R / A  persistent lane refill over pixel chunks; A amortises
+//                             the escape test (block-end test + exact replay)
+//   colorize_kernel           count -> RGBA colour levels (HBM-bound)
+// All iteration goes through Iter<T, STRICT>::step / core or the PTX vote loops, which
+// implement the same operation sequences (FAST: doubled state, FMA-contracted; STRICT:
+// reading c-9's sequence), so counts do not depend on the kernel.
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -1098,7 +1111,6 @@ struct Workspace {
   unsigned int pad[30];
 };
 
-// Continuation of an in-flight pixel (kernel R's end-of-supply hand-off, see below).
 template <class T, bool STRICT, bool MANDEL, bool COLOR, bool AMORT, int K, int TH>
 __global__ void __launch_bounds__(kThreads)
 escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Workspace* ws,
