@@ -434,14 +434,26 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   return cudaSuccess;
 }
 
+#ifndef FR_P2_K  // compile-time knobs for same-box A/B (tools/ab_build.sh)
+#define FR_P2_K 32
+#endif
+#ifndef FR_P2_K_STRICT
+#define FR_P2_K_STRICT 32
+#endif
+#ifndef FR_P2_TH
+#define FR_P2_TH 8
+#endif
 template <bool MANDEL, bool COLOR>
 cudaError_t launch_twophase_mode(fr_mode mode, const fr::Geom& g, const fr::Palette& pal,
                                  double2 c, cudaStream_t s) {
   switch (mode) {
-    // P2 blocks of 16, service threshold 8 (cfg3 sweep: 32,8 equal; 16,4 / 8,4 / 16,2
-    // 4-12% slower: more refills)
-    case FR_FP32_FAST: return launch_twophase_t<float, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
-    case FR_FP32_STRICT: return launch_twophase_t<float, true, MANDEL, COLOR, 16, 8>(g, pal, c, s);
+    // P2 blocks of 32, service threshold 8 (cfg3 sweep at 2 CTAs/SM with the dry-queue
+    // drain: 32,8 0.1925 ms; 24,8 0.1926; 64,8 0.1929; 32,12 0.1937; 32,6 0.1940;
+    // 16,8 0.1966; 32,4 0.1989; 16,4 0.2062; 8,8 0.2112.  Strict: 32 0.234, 16 0.241)
+    case FR_FP32_FAST:
+      return launch_twophase_t<float, false, MANDEL, COLOR, FR_P2_K, FR_P2_TH>(g, pal, c, s);
+    case FR_FP32_STRICT:
+      return launch_twophase_t<float, true, MANDEL, COLOR, FR_P2_K_STRICT, FR_P2_TH>(g, pal, c, s);
     case FR_FP64_FAST: return launch_twophase_t<double, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
     case FR_FP64_STRICT: return launch_twophase_t<double, true, MANDEL, COLOR, 16, 8>(g, pal, c, s);
   }
