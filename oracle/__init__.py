@@ -83,6 +83,16 @@ def _load():
         lib.oracle_escape_fn_f64.restype = i32
         lib.oracle_julia_fn.argtypes = [i32, f64, f64, f64, f64, f64, f64, i64, i64, i32, i32, vp]
         lib.oracle_julia_fn.restype = i32
+        lib.oracle_escape_fma_f32.argtypes = [f32, f32, f32, f32, i32]
+        lib.oracle_escape_fma_f32.restype = i32
+        lib.oracle_escape_fma_f64.argtypes = [f64, f64, f64, f64, i32]
+        lib.oracle_escape_fma_f64.restype = i32
+        lib.oracle_frame_fma.argtypes = [i32, f64, f64, f64, f64, f64, f64, i64, i64, i32, i32,
+                                         vp, i32]
+        lib.oracle_frame_fma.restype = i32
+        lib.oracle_pixels_fma.argtypes = [i32, f64, f64, f64, f64, f64, f64, i64, i64, i32, i32,
+                                          vp, vp, i64, vp, i32]
+        lib.oracle_pixels_fma.restype = i32
         _lib = lib
         return lib
 
@@ -121,11 +131,16 @@ def pixel_to_complex(center: complex, half_w: float, half_h: float, width: int, 
                    lib.oracle_pixel_im(center.imag, half_h, height, py))
 
 
-def escape_time(z0: complex, c: complex, max_iter: int = 100, precision=64) -> int:
+def escape_time(z0: complex, c: complex, max_iter: int = 100, precision=64,
+                fast: bool = False) -> int:
     """Smallest n in [0, max_iter-1] with |Z_n|^2 > 4, else max_iter.
-    For precision 32 the inputs are rounded to binary32 first."""
+    For precision 32 the inputs are rounded to binary32 first.  fast=True iterates the
+    FMA-contracted sequence that defines the *_FAST modes (reading c-10)."""
     lib = _load()
-    f = lib.oracle_escape_f32 if _prec(precision) == 32 else lib.oracle_escape_f64
+    if fast:
+        f = lib.oracle_escape_fma_f32 if _prec(precision) == 32 else lib.oracle_escape_fma_f64
+    else:
+        f = lib.oracle_escape_f32 if _prec(precision) == 32 else lib.oracle_escape_f64
     return int(f(z0.real, z0.imag, c.real, c.imag, int(max_iter)))
 
 
@@ -142,9 +157,13 @@ def _ptr(a: np.ndarray):
 
 
 def julia(c: complex, center: complex, half_w: float, half_h: float, width: int, height: int,
-          max_iter: int = 100, precision=32, threads: int | None = None) -> np.ndarray:
+          max_iter: int = 100, precision=32, threads: int | None = None,
+          fast: bool = False) -> np.ndarray:
     """Julia frame of Z^2 + C: uint16 counts [height, width], row 0 = top."""
     out = np.empty((height, width), dtype=np.uint16)
+    if fast:
+        return _frame_fma(0, c, center, half_w, half_h, width, height, max_iter, precision,
+                          threads, out)
     rc = _load().oracle_julia(c.real, c.imag, center.real, center.imag, half_w, half_h, width,
                               height, max_iter, _prec(precision), _ptr(out),
                               threads or default_threads())
@@ -154,9 +173,13 @@ def julia(c: complex, center: complex, half_w: float, half_h: float, width: int,
 
 
 def mandelbrot(center: complex, half_w: float, half_h: float, width: int, height: int,
-               max_iter: int = 100, precision=64, threads: int | None = None) -> np.ndarray:
+               max_iter: int = 100, precision=64, threads: int | None = None,
+               fast: bool = False) -> np.ndarray:
     """Mandelbrot parameter map: C from the pixel, Z_0 = 0."""
     out = np.empty((height, width), dtype=np.uint16)
+    if fast:
+        return _frame_fma(1, 0j, center, half_w, half_h, width, height, max_iter, precision,
+                          threads, out)
     rc = _load().oracle_mandel(center.real, center.imag, half_w, half_h, width, height, max_iter,
                                _prec(precision), _ptr(out), threads or default_threads())
     if rc != 0:
@@ -165,7 +188,8 @@ def mandelbrot(center: complex, half_w: float, half_h: float, width: int, height
 
 
 def pixels(kind: str, c: complex, center: complex, half_w: float, half_h: float, width: int,
-           height: int, max_iter: int, precision, px, py, threads: int | None = None) -> np.ndarray:
+           height: int, max_iter: int, precision, px, py, threads: int | None = None,
+           fast: bool = False) -> np.ndarray:
     """Counts of selected pixels (px[i], py[i]) of a width x height grid; kind 'julia' or
     'mandelbrot'.  Lets parity run at full BASELINE sizes on a sample."""
     px = np.ascontiguousarray(px, dtype=np.int64)
@@ -174,11 +198,23 @@ def pixels(kind: str, c: complex, center: complex, half_w: float, half_h: float,
         raise ValueError("px/py shape mismatch")
     out = np.empty(px.shape, dtype=np.uint16)
     mandel = {"julia": 0, "mandelbrot": 1}[kind]
-    rc = _load().oracle_pixels(mandel, c.real, c.imag, center.real, center.imag, half_w, half_h,
-                               width, height, max_iter, _prec(precision), _ptr(px), _ptr(py),
-                               px.size, _ptr(out), threads or default_threads())
+    lib = _load()
+    fn = lib.oracle_pixels_fma if fast else lib.oracle_pixels
+    rc = fn(mandel, c.real, c.imag, center.real, center.imag, half_w, half_h,
+            width, height, max_iter, _prec(precision), _ptr(px), _ptr(py), px.size, _ptr(out),
+            threads or default_threads())
     if rc != 0:
         raise ValueError("oracle_pixels: invalid arguments")
+    return out
+
+
+def _frame_fma(mandel, c, center, half_w, half_h, width, height, max_iter, precision, threads,
+               out):
+    rc = _load().oracle_frame_fma(mandel, c.real, c.imag, center.real, center.imag, half_w,
+                                  half_h, width, height, max_iter, _prec(precision), _ptr(out),
+                                  threads or default_threads())
+    if rc != 0:
+        raise ValueError("oracle_frame_fma: invalid arguments")
     return out
 
 

@@ -11,6 +11,11 @@
  * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared -pthread
  * (FP contraction OFF, no FTZ/DAZ: every +, -, * below is one IEEE-754
  * round-to-nearest-even operation in the declared type.)
+ *
+ * Two operation sequences of the same count definition: the strict one
+ * (oracle_escape_f32/f64, DESIGN.md §2 / reading c-9) and the FAST one
+ * (oracle_escape_fma_f32/f64: explicit C99 fmaf/fma calls, each one correctly
+ * rounded fused operation; reading c-10 and its supplement).
  */
 #include <float.h>
 #include <math.h>
@@ -112,31 +117,76 @@ int oracle_escape_f64(double zre, double zim, double cre, double cim, int max_it
     return max_iter;
 }
 
+/* ------------------------------------------------------------------------- */
+/* FAST-mode escape time: the same count definition with the FMA-contracted  */
+/* operation sequence that defines the *_FAST modes (DESIGN.md §5 "State     */
+/* representation", reading c-10; the paper fixes no contraction, so this    */
+/* sequence is the project's definition of FAST, written here in its natural  */
+/* unscaled form with C99's correctly rounded fmaf/fma):                      */
+/*   yy = y*y; m = fma(x, x, yy); if (m > 4) return n;                        */
+/*   t = fma(x, x, -yy); y = fma(x + x, y, ci); x = t + cr;                   */
+/* (x + x is exact.)  Independent of the GPU code, which keeps the state      */
+/* doubled; the two are equal because every step differs by an exact power   */
+/* of two.                                                                    */
+/* ------------------------------------------------------------------------- */
+
+int oracle_escape_fma_f32(float zre, float zim, float cre, float cim, int max_iter) {
+    float x = zre, y = zim;
+    for (int n = 0; n < max_iter; ++n) {
+        float yy = y * y;
+        float m = fmaf(x, x, yy);
+        if (m > 4.0f) return n;
+        float t = fmaf(x, x, -yy);
+        float yn = fmaf(x + x, y, cim);
+        x = t + cre;
+        y = yn;
+    }
+    return max_iter;
+}
+
+int oracle_escape_fma_f64(double zre, double zim, double cre, double cim, int max_iter) {
+    double x = zre, y = zim;
+    for (int n = 0; n < max_iter; ++n) {
+        double yy = y * y;
+        double m = fma(x, x, yy);
+        if (m > 4.0) return n;
+        double t = fma(x, x, -yy);
+        double yn = fma(x + x, y, cim);
+        x = t + cre;
+        y = yn;
+    }
+    return max_iter;
+}
+
 /* One pixel of a Julia frame (Z_0 from the pixel, fixed C) or of a
  * Mandelbrot parameter map (C from the pixel, Z_0 = 0).  precision is
  * 32 or 64; for 32 the double inputs are rounded to binary32 once (c-8). */
 static int pixel_count_n(int mandel, int precision, double c_re, double c_im,
                          double center_re, double center_im, double half_w, double half_h,
                          int64_t width, int64_t height, int64_t px, int64_t py, int max_iter,
-                         int nudge) {
+                         int nudge, int fast) {
     double re = oracle_pixel_re(center_re, half_w, width, px);
     double im = oracle_pixel_im(center_im, half_h, height, py);
     if (precision == 32) {
+        int (*esc)(float, float, float, float, int) =
+            fast ? oracle_escape_fma_f32 : oracle_escape_f32;
         float r = (float)re;
         for (int k = 0; k < nudge; ++k) r = nextafterf(r, INFINITY);
-        if (mandel) return oracle_escape_f32(0.0f, 0.0f, r, (float)im, max_iter);
-        return oracle_escape_f32(r, (float)im, (float)c_re, (float)c_im, max_iter);
+        if (mandel) return esc(0.0f, 0.0f, r, (float)im, max_iter);
+        return esc(r, (float)im, (float)c_re, (float)c_im, max_iter);
     }
+    int (*esc64)(double, double, double, double, int) =
+        fast ? oracle_escape_fma_f64 : oracle_escape_f64;
     for (int k = 0; k < nudge; ++k) re = nextafter(re, INFINITY);
-    if (mandel) return oracle_escape_f64(0.0, 0.0, re, im, max_iter);
-    return oracle_escape_f64(re, im, c_re, c_im, max_iter);
+    if (mandel) return esc64(0.0, 0.0, re, im, max_iter);
+    return esc64(re, im, c_re, c_im, max_iter);
 }
 
 static int pixel_count(int mandel, int precision, double c_re, double c_im, double center_re,
                        double center_im, double half_w, double half_h, int64_t width,
-                       int64_t height, int64_t px, int64_t py, int max_iter) {
+                       int64_t height, int64_t px, int64_t py, int max_iter, int fast) {
     return pixel_count_n(mandel, precision, c_re, c_im, center_re, center_im, half_w, half_h,
-                         width, height, px, py, max_iter, 0);
+                         width, height, px, py, max_iter, 0, fast);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -156,6 +206,7 @@ typedef struct {
     int64_t n_pix;
     int64_t next; /* shared work counter */
     int nudge;    /* ulps added to the start value's real part (0 = none) */
+    int fast;     /* 1: the FAST (FMA-contracted) sequence, 0: strict */
 } job_t;
 
 static void* grid_worker(void* arg) {
@@ -166,7 +217,7 @@ static void* grid_worker(void* arg) {
         for (int64_t px = 0; px < j->width; ++px)
             j->out[row * j->width + px] = (uint16_t)pixel_count(
                 j->mandel, j->precision, j->c_re, j->c_im, j->center_re, j->center_im,
-                j->half_w, j->half_h, j->width, j->height, px, row, j->max_iter);
+                j->half_w, j->half_h, j->width, j->height, px, row, j->max_iter, j->fast);
     }
     return NULL;
 }
@@ -182,7 +233,7 @@ static void* list_worker(void* arg) {
             j->out[i] = (uint16_t)pixel_count_n(j->mandel, j->precision, j->c_re, j->c_im,
                                                 j->center_re, j->center_im, j->half_w,
                                                 j->half_h, j->width, j->height, j->px[i],
-                                                j->py[i], j->max_iter, j->nudge);
+                                                j->py[i], j->max_iter, j->nudge, j->fast);
     }
     return NULL;
 }
@@ -261,6 +312,32 @@ int oracle_pixels_nudged(int mandel, double c_re, double c_im, double center_re,
         if (px[i] < 0 || px[i] >= width || py[i] < 0 || py[i] >= height) return -1;
     job_t j = {mandel ? 1 : 0, precision, max_iter, c_re, c_im, center_re, center_im, half_w,
                half_h, width, height, out, px, py, n_pix, 0, nudge};
+    return run_threads(&j, threads, list_worker);
+}
+
+/* FAST-mode frames and sampled pixels (oracle_escape_fma_*): the same grids and
+ * start values as oracle_julia / oracle_mandel / oracle_pixels, iterated with the
+ * FMA-contracted sequence that defines the *_FAST modes.  mandel selects the map. */
+int oracle_frame_fma(int mandel, double c_re, double c_im, double center_re,
+                     double center_im, double half_w, double half_h, int64_t width,
+                     int64_t height, int max_iter, int precision, uint16_t* out, int threads) {
+    if (!args_ok(precision, width, height, max_iter) || !out) return -1;
+    job_t j = {mandel ? 1 : 0, precision, max_iter, c_re, c_im, center_re, center_im, half_w,
+               half_h, width, height, out, NULL, NULL, 0, 0, 0, 1};
+    return run_threads(&j, threads, grid_worker);
+}
+
+int oracle_pixels_fma(int mandel, double c_re, double c_im, double center_re,
+                      double center_im, double half_w, double half_h, int64_t width,
+                      int64_t height, int max_iter, int precision, const int64_t* px,
+                      const int64_t* py, int64_t n_pix, uint16_t* out, int threads) {
+    if (!args_ok(precision, width, height, max_iter) || n_pix < 0) return -1;
+    if (n_pix == 0) return 0;
+    if (!px || !py || !out) return -1;
+    for (int64_t i = 0; i < n_pix; ++i)
+        if (px[i] < 0 || px[i] >= width || py[i] < 0 || py[i] >= height) return -1;
+    job_t j = {mandel ? 1 : 0, precision, max_iter, c_re, c_im, center_re, center_im, half_w,
+               half_h, width, height, out, px, py, n_pix, 0, 0, 1};
     return run_threads(&j, threads, list_worker);
 }
 
