@@ -935,7 +935,11 @@ escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
   }
 }
 
-template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH>
+// AMORT (P2 only, under the escape-monotonicity precondition |C| <= 1.989 checked on the
+// host): blocks run the bare Z^2+C core and test |Z|^2 once at the block end; a finished
+// lane recovers its exact index by replaying its last block from the saved start state
+// with the per-iteration test, when the warp services it (as kernel A).
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH, bool AMORT = false>
 __global__ void __launch_bounds__(kThreads)
 escape_cont_kernel(const Geom g, const Palette pal, const T jcr, const T jci, ContQueue* q,
                    const QItem<T>* items) {
@@ -1035,6 +1039,53 @@ escape_cont_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Co
     const int n_held = __popc(__ballot_sync(kFull, off >= 0));
     if (n_held == 0) break;
     const bool held = off >= 0;
+    if constexpr (AMORT) {
+      // cnt = iterations done; Z_cnt (= (x, y)) not yet tested.  A finished lane freezes
+      // (x0, y0, cnt) until it is serviced.  Once the queue is dry the warp runs until
+      // every held lane has finished and services them all at once.
+      const int thr = exhausted ? n_held : (TH < n_held ? TH : n_held);
+      bool done = !held, esc = false;
+      T x0 = x, y0 = y;
+      unsigned fm;
+      for (;;) {
+        if (!done) {
+          x0 = x;
+          y0 = y;
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) It::core(x, y, cr, ci);
+        const bool e = !(It::mag(x, y) <= It::kLim);  // unordered: NaN/inf count as escaped
+        if (!done && (e || cnt + K >= max_iter)) {
+          done = true;
+          esc = e;
+        }
+        if (!done) cnt += K;
+        fm = __ballot_sync(kFull, held && done);
+        if (__popc(fm) >= thr) break;
+      }
+      if (held && done) {
+        // exact index: replay the block from its start state with the per-iteration
+        // test, in sub-blocks of 4 until every replaying lane has escaped
+        T rx = x0, ry = y0;
+        unsigned ra = 1u;
+        int rc = 0;
+        for (int j = 0; j < K; j += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) It::step(rx, ry, cr, ci, ra, rc);
+          if (!__any_sync(fm, ra)) break;
+        }
+        // rc < K: escaped at cnt + rc; rc == K: at the block-end state (cnt + K) if
+        // `esc`, else the iteration limit was reached without escape
+        const int count0 = esc ? cnt + rc : max_iter;
+        const int count = count0 < max_iter ? count0 : max_iter;
+        g.counts[off] = (uint16_t)count;
+        if (COLOR) g.rgba[off] = colour_of(spal, pal, count, max_iter);
+        off = -1;
+      }
+      if (exhausted) break;
+      need = fm;
+      continue;
+    }
     if (exhausted) {
       // Queue dry: nothing left to refill, so no per-lane servicing -- run blocks until
       // no held orbit is still alive below max_iter (one vote per block), then store all.

@@ -371,17 +371,18 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
 std::map<std::pair<int, uintptr_t>, std::pair<void*, size_t>> g_queue, g_items;
 constexpr int64_t kTwoPhaseMaxPixels = int64_t(1) << 25;  // item buffer <= 1 GiB (fp64)
 
-int twophase_budget() {  // FRACTAL_BUDGET (multiple of 4), default 96
-  static const int b = [] {
-    const int v = env_int("FRACTAL_BUDGET", 96);
-    return v < 4 ? 4 : v - v % 4;
-  }();
-  return b;
+// P1's budget (FRACTAL_BUDGET, multiple of 4): 96 before an exact P2, 64 before the
+// amortised P2, whose iterations are cheaper (cfg3 fast, 3 CTAs/SM: 32/48/64/80
+// 0.1812-0.1823/0.1812/0.1809/0.1823 ms)
+int twophase_budget(bool amort) {
+  static const int b = env_int("FRACTAL_BUDGET", 0);
+  const int v = b > 0 ? b : (amort ? 64 : 96);
+  return v < 4 ? 4 : v - v % 4;
 }
 
-template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH>
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH, int KA, int THA>
 cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double2 c,
-                              cudaStream_t s) {
+                              cudaStream_t s, bool amort) {
   fr::Geom g = g0;
   const T jcr = MANDEL ? T(0) : state_of<T, STRICT>(c.x);
   const T jci = MANDEL ? T(0) : state_of<T, STRICT>(c.y);
@@ -404,24 +405,35 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   auto* items = static_cast<fr::QItem<T>*>(ip);
   const dim3 grid1 = tile_grid(g, (g.rows + 2 * fr::kTileH - 1) / (2 * fr::kTileH), 1);
   fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR>
-      <<<grid1, fr::kThreads, 0, s>>>(g, pal, jcr, jci, twophase_budget(), q, items);
+      <<<grid1, fr::kThreads, 0, s>>>(g, pal, jcr, jci, twophase_budget(amort), q, items);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  auto kern = fr::escape_cont_kernel<T, STRICT, MANDEL, COLOR, K, TH>;
+  // P2 with the amortised block-end test when the escape-monotonicity precondition
+  // holds (host-checked), else the exact per-iteration test
+  auto kern = amort ? fr::escape_cont_kernel<T, STRICT, MANDEL, COLOR, KA, THA, true>
+                    : fr::escape_cont_kernel<T, STRICT, MANDEL, COLOR, K, TH, false>;
   static const int occ = [&] {
-    int o = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, fr::kThreads, 0) != cudaSuccess ||
-        o <= 0)
+    int o = 0, oa = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &o, fr::escape_cont_kernel<T, STRICT, MANDEL, COLOR, K, TH, false>, fr::kThreads,
+            0) != cudaSuccess || o <= 0)
       o = 1;
-    return o;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &oa, fr::escape_cont_kernel<T, STRICT, MANDEL, COLOR, KA, THA, true>, fr::kThreads,
+            0) != cudaSuccess || oa <= 0)
+      oa = 1;
+    return o < oa ? o : oa;
   }();
   // P2 runs 2 CTAs per SM (FRACTAL_P2_OCC), not the occupancy limit: a few warps per
   // SMSP already saturate issue for this loop, and every extra resident lane only adds
   // to the work still in flight when the queue runs dry (cfg3: 8 CTAs 0.273 ms, 3 CTAs
   // 0.1975, 2 CTAs 0.1965; strict 0.250 vs 0.246)
-  static const int occ_env = env_int("FRACTAL_P2_OCC", 2);
-  const int occ2 = occ_env > 0 && occ_env < occ ? occ_env : occ;
+  // The amortised P2 issues fewer instructions per iteration and runs best at 3 CTAs/SM
+  // (cfg3 fast at budget 64: 2/3/4 CTAs 0.1846/0.1809/0.1842 ms)
+  static const int occ_env = env_int("FRACTAL_P2_OCC", 0);
+  const int occ_want = occ_env > 0 ? occ_env : (amort ? 3 : 2);
+  const int occ2 = occ_want < occ ? occ_want : occ;
   kern<<<(unsigned)(sm_count() * occ2), fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -443,21 +455,41 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
 #ifndef FR_P2_TH
 #define FR_P2_TH 8
 #endif
+#ifndef FR_P2A_K  // amortised P2 (block, service threshold): cfg3 fast sweep, DESIGN §5.1c
+#define FR_P2A_K 24
+#endif
+#ifndef FR_P2A_TH
+#define FR_P2A_TH 16
+#endif
 template <bool MANDEL, bool COLOR>
 cudaError_t launch_twophase_mode(fr_mode mode, const fr::Geom& g, const fr::Palette& pal,
-                                 double2 c, cudaStream_t s) {
+                                 double2 c, cudaStream_t s, bool amort) {
   switch (mode) {
     // P2 blocks of 32, service threshold 8 (cfg3 sweep at 2 CTAs/SM with the dry-queue
     // drain: 32,8 0.1925 ms; 24,8 0.1926; 64,8 0.1929; 32,12 0.1937; 32,6 0.1940;
     // 16,8 0.1966; 32,4 0.1989; 16,4 0.2062; 8,8 0.2112.  Strict: 32 0.234, 16 0.241)
     case FR_FP32_FAST:
-      return launch_twophase_t<float, false, MANDEL, COLOR, FR_P2_K, FR_P2_TH>(g, pal, c, s);
+      return launch_twophase_t<float, false, MANDEL, COLOR, FR_P2_K, FR_P2_TH, FR_P2A_K,
+                               FR_P2A_TH>(g, pal, c, s, amort);
+    // strict: the replayed 7-op step makes the amortised P2 slower (cfg3 0.2417 vs 0.2339
+    // ms at 32,16), so strict modes keep the exact per-iteration test
     case FR_FP32_STRICT:
-      return launch_twophase_t<float, true, MANDEL, COLOR, FR_P2_K_STRICT, FR_P2_TH>(g, pal, c, s);
-    case FR_FP64_FAST: return launch_twophase_t<double, false, MANDEL, COLOR, 16, 8>(g, pal, c, s);
-    case FR_FP64_STRICT: return launch_twophase_t<double, true, MANDEL, COLOR, 16, 8>(g, pal, c, s);
+      return launch_twophase_t<float, true, MANDEL, COLOR, FR_P2_K_STRICT, FR_P2_TH, FR_P2A_K,
+                               FR_P2A_TH>(g, pal, c, s, false);
+    case FR_FP64_FAST:
+      return launch_twophase_t<double, false, MANDEL, COLOR, 16, 8, 16, 16>(g, pal, c, s, amort);
+    case FR_FP64_STRICT:
+      return launch_twophase_t<double, true, MANDEL, COLOR, 16, 8, 16, 16>(g, pal, c, s, false);
   }
   return cudaErrorInvalidValue;
+}
+
+// Amortised P2 for the fast modes when the escape-monotonicity precondition holds
+// (monotone_ok, below); FRACTAL_P2_AMORT=0 keeps the exact per-iteration test.
+bool monotone_ok(bool mandel, fr_complex c, fr_window w);
+bool p2_amort(fr_mode mode, bool mandel, fr_complex c, fr_window w) {
+  static const bool on = env_int("FRACTAL_P2_AMORT", 1) != 0;
+  return on && (mode == FR_FP32_FAST || mode == FR_FP64_FAST) && monotone_ok(mandel, c, w);
 }
 
 // Kernel R: blocks of 16, service threshold 8 (cfg3 sweep: K 8-32 and
@@ -560,14 +592,16 @@ fr_status render_frame(bool mandel, fr_complex c, fr_window win, int32_t width, 
       else
         e = col ? launch_amort_mode<false, true>(mode, g, p, cc, stream)
                 : launch_amort_mode<false, false>(mode, g, p, cc, stream);
-    } else if (sched == kTwoPhase && max_iter > twophase_budget() &&
+    } else if (sched == kTwoPhase &&
+               max_iter > twophase_budget(p2_amort(mode, mandel, c, win)) &&
                (int64_t)g.rows * g.W <= kTwoPhaseMaxPixels) {
+      const bool am = p2_amort(mode, mandel, c, win);
       if (mandel)
-        e = col ? launch_twophase_mode<true, true>(mode, g, p, cc, stream)
-                : launch_twophase_mode<true, false>(mode, g, p, cc, stream);
+        e = col ? launch_twophase_mode<true, true>(mode, g, p, cc, stream, am)
+                : launch_twophase_mode<true, false>(mode, g, p, cc, stream, am);
       else
-        e = col ? launch_twophase_mode<false, true>(mode, g, p, cc, stream)
-                : launch_twophase_mode<false, false>(mode, g, p, cc, stream);
+        e = col ? launch_twophase_mode<false, true>(mode, g, p, cc, stream, am)
+                : launch_twophase_mode<false, false>(mode, g, p, cc, stream, am);
     } else if (mandel) {
       e = col ? launch_refill_mode<true, true>(mode, g, p, cc, stream)
               : launch_refill_mode<true, false>(mode, g, p, cc, stream);

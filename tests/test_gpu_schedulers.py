@@ -59,8 +59,11 @@ def test_fast_mode_identical_across_schedulers():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     hashes = {}
-    for sched in ("static", "refill", "twophase", "amort"):
-        e = dict(os.environ, FRACTAL_SCHED=sched)
+    for sched in ("static", "refill", "twophase", "twophase_exact", "amort"):
+        # twophase: amortised P2 where the precondition holds; twophase_exact: P2 with
+        # the per-iteration test
+        e = dict(os.environ, FRACTAL_SCHED=sched.split("_")[0],
+                 FRACTAL_P2_AMORT="0" if sched.endswith("exact") else "1")
         r = subprocess.run([sys.executable, "-c", _HASH_SCRIPT], cwd=ROOT, env=e,
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
@@ -68,3 +71,24 @@ def test_fast_mode_identical_across_schedulers():
     ref = hashes["static"]
     for sched, h in hashes.items():
         assert h == ref, (sched, h, ref)
+
+
+@pytest.mark.parametrize("env", [{"FRACTAL_SCHED": "twophase"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P2_AMORT": "0"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_BUDGET": "8",
+                                  "FRACTAL_P2_OCC": "1"},
+                                 {"FRACTAL_SCHED": "refill"}, {"FRACTAL_SCHED": "amort"},
+                                 {"FRACTAL_SCHED": "static"}])
+def test_fast_exact_under_forced_scheduler(env):
+    """FAST counts equal the FAST oracle bit for bit under every kernel family, including
+    P2 with the amortised block-end test and with the exact test."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-m", "pytest",
+                        os.path.join(ROOT, "tests", "test_gpu_fast_exact.py"), "-m", "gpu", "-q",
+                        "-x", "-k", "fast_configs or fast_fuzz or fast_mandelbrot",
+                        "-p", "no:cacheprovider"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
