@@ -20,6 +20,10 @@
 #include <type_traits>
 #include <cuda_runtime.h>
 
+#ifndef FR_P2A_KS  // amortised P2: iterations per checkpointed sub-block
+#define FR_P2A_KS 8
+#endif
+
 namespace fr {
 
 constexpr int kThreads = 256;      // 8 warps per CTA
@@ -1044,16 +1048,29 @@ escape_cont_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Co
       // (x0, y0, cnt) until it is serviced.  Once the queue is dry the warp runs until
       // every held lane has finished and services them all at once.
       const int thr = exhausted ? n_held : (TH < n_held ? TH : n_held);
+      // the block is NS sub-blocks of KS iterations; each sub-block's start state is
+      // checkpointed, so the replay covers one sub-block, not the whole block
+      constexpr int KS = (K % FR_P2A_KS == 0) ? FR_P2A_KS : K;
+      constexpr int NS = K / KS;
+      static_assert(KS % 2 == 0, "the replay runs pairs of steps");
       bool done = !held, esc = false;
-      T x0 = x, y0 = y;
+      T xs[NS], ys[NS];
+#pragma unroll
+      for (int sb = 0; sb < NS; ++sb) {
+        xs[sb] = x;
+        ys[sb] = y;
+      }
       unsigned fm;
       for (;;) {
-        if (!done) {
-          x0 = x;
-          y0 = y;
-        }
 #pragma unroll
-        for (int j = 0; j < K; ++j) It::core(x, y, cr, ci);
+        for (int sb = 0; sb < NS; ++sb) {
+          if (!done) {
+            xs[sb] = x;
+            ys[sb] = y;
+          }
+#pragma unroll
+          for (int j = 0; j < KS; ++j) It::core(x, y, cr, ci);
+        }
         const bool e = !(It::mag(x, y) <= It::kLim);  // unordered: NaN/inf count as escaped
         if (!done && (e || cnt + K >= max_iter)) {
           done = true;
@@ -1064,19 +1081,29 @@ escape_cont_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Co
         if (__popc(fm) >= thr) break;
       }
       if (held && done) {
-        // exact index: replay the block from its start state with the per-iteration
-        // test, in sub-blocks of 4 until every replaying lane has escaped
-        T rx = x0, ry = y0;
+        // exact index: the first sub-block whose end state escaped (monotonicity: every
+        // later state escaped too), replayed from its checkpoint with the per-iteration
+        // test until every replaying lane has escaped
+        T rx = xs[NS - 1], ry = ys[NS - 1];
+        int sbase = (NS - 1) * KS;
+#pragma unroll
+        for (int sb = NS - 2; sb >= 0; --sb) {
+          if (!(It::mag(xs[sb + 1], ys[sb + 1]) <= It::kLim)) {
+            rx = xs[sb];
+            ry = ys[sb];
+            sbase = sb * KS;
+          }
+        }
         unsigned ra = 1u;
         int rc = 0;
-        for (int j = 0; j < K; j += 4) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) It::step(rx, ry, cr, ci, ra, rc);
+        for (int j = 0; j < KS; j += 2) {
+          It::step(rx, ry, cr, ci, ra, rc);
+          It::step(rx, ry, cr, ci, ra, rc);
           if (!__any_sync(fm, ra)) break;
         }
-        // rc < K: escaped at cnt + rc; rc == K: at the block-end state (cnt + K) if
+        // rc < KS: escaped at cnt + sbase + rc; rc == KS: at the sub-block's end state if
         // `esc`, else the iteration limit was reached without escape
-        const int count0 = esc ? cnt + rc : max_iter;
+        const int count0 = esc ? cnt + sbase + rc : max_iter;
         const int count = count0 < max_iter ? count0 : max_iter;
         g.counts[off] = (uint16_t)count;
         if (COLOR) g.rgba[off] = colour_of(spal, pal, count, max_iter);

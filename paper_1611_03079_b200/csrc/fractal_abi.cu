@@ -371,12 +371,12 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
 std::map<std::pair<int, uintptr_t>, std::pair<void*, size_t>> g_queue, g_items;
 constexpr int64_t kTwoPhaseMaxPixels = int64_t(1) << 25;  // item buffer <= 1 GiB (fp64)
 
-// P1's budget (FRACTAL_BUDGET, multiple of 4): 96 before an exact P2, 64 before the
-// amortised P2, whose iterations are cheaper (cfg3 fast, 3 CTAs/SM: 32/48/64/80
-// 0.1812-0.1823/0.1812/0.1809/0.1823 ms)
+// P1's budget (FRACTAL_BUDGET, multiple of 4): 96 before an exact P2, 48 before the
+// amortised P2, whose iterations are cheaper (cfg3 fast, 3 CTAs/SM, K 64: 48/64/96
+// 0.1679/0.1685/0.1719 ms)
 int twophase_budget(bool amort) {
   static const int b = env_int("FRACTAL_BUDGET", 0);
-  const int v = b > 0 ? b : (amort ? 64 : 96);
+  const int v = b > 0 ? b : (amort ? 48 : 96);
   return v < 4 ? 4 : v - v % 4;
 }
 
@@ -430,7 +430,7 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   // to the work still in flight when the queue runs dry (cfg3: 8 CTAs 0.273 ms, 3 CTAs
   // 0.1975, 2 CTAs 0.1965; strict 0.250 vs 0.246)
   // The amortised P2 issues fewer instructions per iteration and runs best at 3 CTAs/SM
-  // (cfg3 fast at budget 64: 2/3/4 CTAs 0.1846/0.1809/0.1842 ms)
+  // (cfg3 fast, K 64: 2/3/4 CTAs 0.1704/0.1687/0.1715 ms)
   static const int occ_env = env_int("FRACTAL_P2_OCC", 0);
   const int occ_want = occ_env > 0 ? occ_env : (amort ? 3 : 2);
   const int occ2 = occ_want < occ ? occ_want : occ;
@@ -456,10 +456,10 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
 #define FR_P2_TH 8
 #endif
 #ifndef FR_P2A_K  // amortised P2 (block, service threshold): cfg3 fast sweep, DESIGN §5.1c
-#define FR_P2A_K 24
+#define FR_P2A_K 64   // with checkpointed sub-blocks of FR_P2A_KS = 8 (escape_kernels.cuh)
 #endif
 #ifndef FR_P2A_TH
-#define FR_P2A_TH 16
+#define FR_P2A_TH 12
 #endif
 template <bool MANDEL, bool COLOR>
 cudaError_t launch_twophase_mode(fr_mode mode, const fr::Geom& g, const fr::Palette& pal,
