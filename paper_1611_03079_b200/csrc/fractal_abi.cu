@@ -411,18 +411,24 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   g_launches.fetch_add(1, std::memory_order_relaxed);
   // P2 with the amortised block-end test when the escape-monotonicity precondition
   // holds (host-checked), else the exact per-iteration test
-  auto kern = amort ? fr::escape_cont_kernel<T, STRICT, MANDEL, COLOR, KA, THA, true>
-                    : fr::escape_cont_kernel<T, STRICT, MANDEL, COLOR, K, TH, false>;
+  // (strict modes never take the amortised kernel: it is not instantiated for them)
+  auto kern = fr::escape_cont_kernel<T, STRICT, MANDEL, COLOR, K, TH, false>;
+  if constexpr (!STRICT) {
+    if (amort) kern = fr::escape_cont_kernel<T, STRICT, MANDEL, COLOR, KA, THA, true>;
+  }
   static const int occ = [&] {
     int o = 0, oa = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &o, fr::escape_cont_kernel<T, STRICT, MANDEL, COLOR, K, TH, false>, fr::kThreads,
             0) != cudaSuccess || o <= 0)
       o = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &oa, fr::escape_cont_kernel<T, STRICT, MANDEL, COLOR, KA, THA, true>, fr::kThreads,
-            0) != cudaSuccess || oa <= 0)
-      oa = 1;
+    oa = o;
+    if constexpr (!STRICT) {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+              &oa, fr::escape_cont_kernel<T, STRICT, MANDEL, COLOR, KA, THA, true>,
+              fr::kThreads, 0) != cudaSuccess || oa <= 0)
+        oa = 1;
+    }
     return o < oa ? o : oa;
   }();
   // P2 runs 2 CTAs per SM (FRACTAL_P2_OCC), not the occupancy limit: a few warps per
