@@ -467,6 +467,12 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
 #ifndef FR_P2A_TH
 #define FR_P2A_TH 12
 #endif
+#ifndef FR_P2A_K_F64
+#define FR_P2A_K_F64 32  // cfg3 FP64_FAST: 16,12 0.2566; 32,12 0.2467; 32,16 0.2523; 64,12 0.2473 ms
+#endif
+#ifndef FR_P2A_TH_F64
+#define FR_P2A_TH_F64 12
+#endif
 template <bool MANDEL, bool COLOR>
 cudaError_t launch_twophase_mode(fr_mode mode, const fr::Geom& g, const fr::Palette& pal,
                                  double2 c, cudaStream_t s, bool amort) {
@@ -483,7 +489,8 @@ cudaError_t launch_twophase_mode(fr_mode mode, const fr::Geom& g, const fr::Pale
       return launch_twophase_t<float, true, MANDEL, COLOR, FR_P2_K_STRICT, FR_P2_TH, FR_P2A_K,
                                FR_P2A_TH>(g, pal, c, s, false);
     case FR_FP64_FAST:
-      return launch_twophase_t<double, false, MANDEL, COLOR, 16, 8, 16, 16>(g, pal, c, s, amort);
+      return launch_twophase_t<double, false, MANDEL, COLOR, 16, 8, FR_P2A_K_F64, FR_P2A_TH_F64>(
+          g, pal, c, s, amort);
     case FR_FP64_STRICT:
       return launch_twophase_t<double, true, MANDEL, COLOR, 16, 8, 16, 16>(g, pal, c, s, false);
   }
