@@ -8,7 +8,9 @@
 //   escape_tile2_kernel   S2  one fp32 frame, two pixels per thread
 //   escape_budget_kernel  P1  heavy-tailed frames: static pass up to a budget, survivors
 //                             appended to a queue
-//   escape_cont_kernel    P2  persistent lane refill over P1's survivors
+//   escape_cont_kernel    P2  persistent lane refill over P1's survivors; fast modes with
+//                             |C| <= 1.989 amortise the escape test (block-end test,
+//                             checkpointed sub-blocks, exact replay of one sub-block)
 //   escape_refill_kernel  R / A  persistent lane refill over pixel chunks; A amortises
 //                             the escape test (block-end test + exact replay)
 //   colorize_kernel           count -> RGBA colour levels (HBM-bound)

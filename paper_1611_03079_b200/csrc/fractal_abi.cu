@@ -551,8 +551,10 @@ bool monotone_ok(bool mandel, fr_complex c, fr_window w) {
   return true;
 }
 
-// Scheduling policy for single frames: FRACTAL_SCHED=static|refill overrides; default
-// refill for max_iter >= 256 (heavy-tailed counts), static otherwise.
+// Scheduling policy for single frames (DESIGN.md §5 dispatch table):
+// FRACTAL_SCHED=static|refill|amort|twophase overrides; default static for max_iter <
+// 256, kernel A for deep Mandelbrot maps under the monotonicity precondition, else the
+// two phases (P1 + P2; kernel R for frames too large for the survivor buffer).
 enum Sched { kStatic = 0, kRefill = 1, kAmort = 2, kTwoPhase = 3 };
 
 Sched choose_sched(bool mandel, fr_complex c, fr_window w, int max_iter) {
