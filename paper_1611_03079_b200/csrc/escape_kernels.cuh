@@ -853,7 +853,13 @@ struct ContQueue {
   unsigned pad2[31];
 };
 
-template <class T, bool STRICT, bool MANDEL, bool COLOR>
+// KS > 0 (fast modes, under the escape-monotonicity precondition of kernel A / the
+// amortised P2): sub-blocks of KS bare Z^2+C steps with one |Z|^2 test at the sub-block
+// end; each orbit keeps the start state of its current sub-block until an end state has
+// escaped, and escaped orbits recover their exact index by one replay of <= KS steps
+// with the per-iteration test after the loop (P1's lanes are never refilled, so one
+// replay per orbit, deferred to the end).
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int KS = 0>
 __global__ void __launch_bounds__(kThreads)
 escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, int budget,
                      ContQueue* q, QItem<T>* items) {
@@ -889,8 +895,55 @@ escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
   }
   unsigned alive = in0 ? 1u : 0u, alive2 = in1 ? 1u : 0u;
   int cnt = 0, cnt2 = 0;
-  // budget is a multiple of 4 and < max_iter (host)
-  if constexpr (kAsmPair<T, STRICT, 4>) {
+  // budget is a multiple of 4 (of KS when KS > 0) and < max_iter (host)
+  if constexpr (KS > 0) {
+    static_assert(!STRICT && KS % 2 == 0, "amortised P1: fast modes, pairs of replay steps");
+    using It = Iter<T, STRICT>;
+    // d: the end state of some sub-block escaped (sticky; NaN/inf count as escaped);
+    // (xc, yc) = start state of the first such sub-block, cnt = its first index
+    bool d0 = !in0, d1 = !in1;
+    T xc = x, yc = y, xc2 = x2, yc2 = y2;
+    for (int n = 0; n < budget; n += KS) {
+      if (!d0) {
+        xc = x;
+        yc = y;
+        cnt = n;
+      }
+      if (!d1) {
+        xc2 = x2;
+        yc2 = y2;
+        cnt2 = n;
+      }
+#pragma unroll
+      for (int j = 0; j < KS; ++j) {
+        It::core(x, y, cr, ci);
+        It::core(x2, y2, cr2, ci2);
+      }
+      d0 = d0 || !(It::mag(x, y) <= It::kLim);
+      d1 = d1 || !(It::mag(x2, y2) <= It::kLim);
+      if (__all_sync(kFull, d0 && d1)) break;
+    }
+    // survivors: |Z_budget|^2 <= 4, so (monotonicity) every earlier state passed too
+    if (in0 && !d0) cnt = budget;
+    if (in1 && !d1) cnt2 = budget;
+    alive = (in0 && !d0) ? 1u : 0u;
+    alive2 = (in1 && !d1) ? 1u : 0u;
+    // exact index of the escaped orbits: replay their sub-block from its checkpoint;
+    // rc tests passed before the first escaping state (rc == KS: the end state)
+    unsigned ra = (in0 && d0) ? 1u : 0u, rb = (in1 && d1) ? 1u : 0u;
+    int rc = 0, rc2 = 0;
+    if (__any_sync(kFull, ra | rb)) {
+      for (int j = 0; j < KS; j += 2) {
+        It::step(xc, yc, cr, ci, ra, rc);
+        It::step(xc2, yc2, cr2, ci2, rb, rc2);
+        It::step(xc, yc, cr, ci, ra, rc);
+        It::step(xc2, yc2, cr2, ci2, rb, rc2);
+        if (!__any_sync(kFull, ra | rb)) break;
+      }
+    }
+    if (!alive) cnt += rc;
+    if (!alive2) cnt2 += rc2;
+  } else if constexpr (kAsmPair<T, STRICT, 4>) {
     vote_loop2_f32<STRICT>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2, budget);
   } else {
     for (int n = 0; n < budget; n += 4) {

@@ -380,6 +380,9 @@ int twophase_budget(bool amort) {
   return v < 4 ? 4 : v - v % 4;
 }
 
+#ifndef FR_P1A_KS  // amortised P1 sub-block (0 = exact per-iteration test)
+#define FR_P1A_KS 0
+#endif
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH, int KA, int THA>
 cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double2 c,
                               cudaStream_t s, bool amort) {
@@ -404,8 +407,18 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   if (e != cudaSuccess) return e;
   auto* items = static_cast<fr::QItem<T>*>(ip);
   const dim3 grid1 = tile_grid(g, (g.rows + 2 * fr::kTileH - 1) / (2 * fr::kTileH), 1);
-  fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR>
-      <<<grid1, fr::kThreads, 0, s>>>(g, pal, jcr, jci, twophase_budget(amort), q, items);
+  const int budget = twophase_budget(amort);
+  // amortised P1 under the same precondition as the amortised P2 (FRACTAL_P1_AMORT:
+  // 0 = exact test, else sub-blocks of 4 or 8 when the budget is a multiple of it)
+  static const int p1ks = env_int("FRACTAL_P1_AMORT", FR_P1A_KS);
+  auto kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR>;
+  if constexpr (!STRICT) {
+    if (amort && p1ks == 4 && budget % 4 == 0)
+      kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 4>;
+    if (amort && p1ks == 8 && budget % 8 == 0)
+      kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 8>;
+  }
+  kern1<<<grid1, fr::kThreads, 0, s>>>(g, pal, jcr, jci, budget, q, items);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -59,11 +59,14 @@ def test_fast_mode_identical_across_schedulers():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     hashes = {}
-    for sched in ("static", "refill", "twophase", "twophase_exact", "amort"):
+    for sched in ("static", "refill", "twophase", "twophase_exact", "twophase_p1a4",
+                  "twophase_p1a8", "amort"):
         # twophase: amortised P2 where the precondition holds; twophase_exact: P2 with
-        # the per-iteration test
+        # the per-iteration test; _p1aK: amortised P1 with sub-blocks of K
         e = dict(os.environ, FRACTAL_SCHED=sched.split("_")[0],
                  FRACTAL_P2_AMORT="0" if sched.endswith("exact") else "1")
+        if "_p1a" in sched:
+            e["FRACTAL_P1_AMORT"] = sched[-1]
         r = subprocess.run([sys.executable, "-c", _HASH_SCRIPT], cwd=ROOT, env=e,
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
@@ -77,6 +80,10 @@ def test_fast_mode_identical_across_schedulers():
                                  {"FRACTAL_SCHED": "twophase", "FRACTAL_P2_AMORT": "0"},
                                  {"FRACTAL_SCHED": "twophase", "FRACTAL_BUDGET": "8",
                                   "FRACTAL_P2_OCC": "1"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_AMORT": "4"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_AMORT": "8"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_AMORT": "8",
+                                  "FRACTAL_BUDGET": "8"},
                                  {"FRACTAL_SCHED": "refill"}, {"FRACTAL_SCHED": "amort"},
                                  {"FRACTAL_SCHED": "static"}])
 def test_fast_exact_under_forced_scheduler(env):
