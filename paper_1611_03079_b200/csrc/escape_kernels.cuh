@@ -859,7 +859,9 @@ struct ContQueue {
 // escaped, and escaped orbits recover their exact index by one replay of <= KS steps
 // with the per-iteration test after the loop (P1's lanes are never refilled, so one
 // replay per orbit, deferred to the end).
-template <class T, bool STRICT, bool MANDEL, bool COLOR, int KS = 0>
+// PRE > 0: the first PRE iterations run the exact vote loop (counts of the orbits that
+// end there are final); the amortised sub-blocks continue the rest from PRE.
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int KS = 0, int PRE = 0>
 __global__ void __launch_bounds__(kThreads)
 escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, int budget,
                      ContQueue* q, QItem<T>* items) {
@@ -899,11 +901,31 @@ escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
   if constexpr (KS > 0) {
     static_assert(!STRICT && KS % 2 == 0, "amortised P1: fast modes, pairs of replay steps");
     using It = Iter<T, STRICT>;
+    // exact prefix of PRE iterations (most orbits of a heavy-tailed frame end there)
+    int n0 = 0;
+    if constexpr (PRE > 0) {
+      if constexpr (kAsmPair<T, STRICT, 4>) {
+        n0 = vote_loop2_f32<STRICT>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2,
+                                    PRE);
+      } else {
+        for (; n0 < PRE; n0 += 4) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            Iter<T, STRICT>::step(x, y, cr, ci, alive, cnt);
+            Iter<T, STRICT>::step(x2, y2, cr2, ci2, alive2, cnt2);
+          }
+          if (!__any_sync(kFull, alive | alive2)) break;
+        }
+      }
+    }
+    // p: still running after the prefix (its count is final otherwise)
+    const bool p0 = alive != 0u, p1 = alive2 != 0u;
     // d: the end state of some sub-block escaped (sticky; NaN/inf count as escaped);
     // (xc, yc) = start state of the first such sub-block, cnt = its first index
-    bool d0 = !in0, d1 = !in1;
+    bool d0 = !p0, d1 = !p1;
     T xc = x, yc = y, xc2 = x2, yc2 = y2;
-    for (int n = 0; n < budget; n += KS) {
+    if (!__any_sync(kFull, p0 || p1)) n0 = budget;
+    for (int n = n0; n < budget; n += KS) {
       if (!d0) {
         xc = x;
         yc = y;
@@ -924,13 +946,15 @@ escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
       if (__all_sync(kFull, d0 && d1)) break;
     }
     // survivors: |Z_budget|^2 <= 4, so (monotonicity) every earlier state passed too
-    if (in0 && !d0) cnt = budget;
-    if (in1 && !d1) cnt2 = budget;
-    alive = (in0 && !d0) ? 1u : 0u;
-    alive2 = (in1 && !d1) ? 1u : 0u;
-    // exact index of the escaped orbits: replay their sub-block from its checkpoint;
-    // rc tests passed before the first escaping state (rc == KS: the end state)
-    unsigned ra = (in0 && d0) ? 1u : 0u, rb = (in1 && d1) ? 1u : 0u;
+    if (!d0) cnt = budget;
+    if (!d1) cnt2 = budget;
+    alive = !d0 ? 1u : 0u;
+    alive2 = !d1 ? 1u : 0u;
+    // exact index of the orbits that escaped after the prefix: replay their sub-block
+    // from its checkpoint; rc tests passed before the first escaping state (rc == KS:
+    // the end state)
+    const bool q0 = p0 && d0, q1 = p1 && d1;
+    unsigned ra = q0 ? 1u : 0u, rb = q1 ? 1u : 0u;
     int rc = 0, rc2 = 0;
     if (__any_sync(kFull, ra | rb)) {
       for (int j = 0; j < KS; j += 2) {
@@ -941,8 +965,8 @@ escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
         if (!__any_sync(kFull, ra | rb)) break;
       }
     }
-    if (!alive) cnt += rc;
-    if (!alive2) cnt2 += rc2;
+    if (q0) cnt += rc;
+    if (q1) cnt2 += rc2;
   } else if constexpr (kAsmPair<T, STRICT, 4>) {
     vote_loop2_f32<STRICT>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2, budget);
   } else {

@@ -383,6 +383,9 @@ int twophase_budget(bool amort) {
 #ifndef FR_P1A_KS  // amortised P1 sub-block (0 = exact per-iteration test)
 #define FR_P1A_KS 0
 #endif
+#ifndef FR_P1A_PRE
+#define FR_P1A_PRE 0
+#endif
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH, int KA, int THA>
 cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double2 c,
                               cudaStream_t s, bool amort) {
@@ -410,13 +413,23 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   const int budget = twophase_budget(amort);
   // amortised P1 under the same precondition as the amortised P2 (FRACTAL_P1_AMORT:
   // 0 = exact test, else sub-blocks of 4 or 8 when the budget is a multiple of it)
+  // FRACTAL_P1_PRE: exact prefix of 0 / 8 / 16 iterations before the amortised blocks
   static const int p1ks = env_int("FRACTAL_P1_AMORT", FR_P1A_KS);
+  static const int p1pre = env_int("FRACTAL_P1_PRE", FR_P1A_PRE);
   auto kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR>;
   if constexpr (!STRICT) {
-    if (amort && p1ks == 4 && budget % 4 == 0)
-      kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 4>;
-    if (amort && p1ks == 8 && budget % 8 == 0)
-      kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 8>;
+    if (amort && budget > p1pre && (budget - p1pre) % 8 == 0) {
+      if (p1ks == 4 && p1pre == 0) kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 4>;
+      if (p1ks == 8 && p1pre == 0) kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 8>;
+      if (p1ks == 4 && p1pre == 8)
+        kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 4, 8>;
+      if (p1ks == 8 && p1pre == 8)
+        kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 8, 8>;
+      if (p1ks == 4 && p1pre == 16)
+        kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 4, 16>;
+      if (p1ks == 8 && p1pre == 16)
+        kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 8, 16>;
+    }
   }
   kern1<<<grid1, fr::kThreads, 0, s>>>(g, pal, jcr, jci, budget, q, items);
   e = cudaGetLastError();

@@ -60,13 +60,15 @@ def test_fast_mode_identical_across_schedulers():
         pytest.skip("no CUDA device")
     hashes = {}
     for sched in ("static", "refill", "twophase", "twophase_exact", "twophase_p1a4",
-                  "twophase_p1a8", "amort"):
+                  "twophase_p1a8", "twophase_p1a8pre16", "amort"):
         # twophase: amortised P2 where the precondition holds; twophase_exact: P2 with
         # the per-iteration test; _p1aK: amortised P1 with sub-blocks of K
         e = dict(os.environ, FRACTAL_SCHED=sched.split("_")[0],
                  FRACTAL_P2_AMORT="0" if sched.endswith("exact") else "1")
         if "_p1a" in sched:
-            e["FRACTAL_P1_AMORT"] = sched[-1]
+            e["FRACTAL_P1_AMORT"] = sched.split("_p1a")[1][0]
+            if "pre" in sched:
+                e["FRACTAL_P1_PRE"] = sched.split("pre")[1]
         r = subprocess.run([sys.executable, "-c", _HASH_SCRIPT], cwd=ROOT, env=e,
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
@@ -84,6 +86,10 @@ def test_fast_mode_identical_across_schedulers():
                                  {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_AMORT": "8"},
                                  {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_AMORT": "8",
                                   "FRACTAL_BUDGET": "8"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_AMORT": "4",
+                                  "FRACTAL_P1_PRE": "8"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_AMORT": "8",
+                                  "FRACTAL_P1_PRE": "16"},
                                  {"FRACTAL_SCHED": "refill"}, {"FRACTAL_SCHED": "amort"},
                                  {"FRACTAL_SCHED": "static"}])
 def test_fast_exact_under_forced_scheduler(env):
