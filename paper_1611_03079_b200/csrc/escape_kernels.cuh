@@ -538,7 +538,9 @@ __device__ __forceinline__ int strict_vote_loop2_f32(float& x, float& y, int& cn
 #undef FR_STRICT_STEP2
 
 // Two-orbit PTX vote loop of either fp32 mode (blocks of 4).
-template <bool STRICT>
+// KV: vote block of the fast loop (4, or 2 for the FRACTAL_VOTE_K=2 experiment; strict
+// always 4); kfull must be a multiple of it
+template <bool STRICT, int KV = 4>
 __device__ __forceinline__ int vote_loop2_f32(float& x, float& y, int& cnt, unsigned& alive,
                                               float& x2, float& y2, int& cnt2, unsigned& alive2,
                                               float cr, float ci, float crb, float cib,
@@ -546,7 +548,7 @@ __device__ __forceinline__ int vote_loop2_f32(float& x, float& y, int& cnt, unsi
   if constexpr (STRICT)
     return strict_vote_loop2_f32(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, crb, cib, kfull);
   else
-    return fast_vote_loop2_f32<4>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, crb, cib, kfull);
+    return fast_vote_loop2_f32<KV>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, crb, cib, kfull);
 }
 
 #undef FR_FAST_STEP2
@@ -754,7 +756,7 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
 // both, half the per-pixel overhead).  Julia frames share C; Mandelbrot maps take each
 // orbit's C from its pixel (Z_0 = 0).  Bit-identical to kernel S (same arithmetic).
 // ----------------------------------------------------------------------------------
-template <bool STRICT, bool MANDEL, bool COLOR>
+template <bool STRICT, bool MANDEL, bool COLOR, int KV = 4>
 __global__ void __launch_bounds__(kThreads)
 escape_tile2_kernel(const Geom g, const Palette pal, const float jcr2, const float jci2) {
   // jcr2/jci2: the Julia C in the state representation (doubled in FAST, plain in STRICT)
@@ -791,8 +793,9 @@ escape_tile2_kernel(const Geom g, const Palette pal, const float jcr2, const flo
   unsigned alive = in0 ? 1u : 0u, alive2 = in1 ? 1u : 0u;
   int cnt = 0, cnt2 = 0;
   const int max_iter = g.max_iter;
-  const int kfull = max_iter - max_iter % 4;
-  int n = vote_loop2_f32<STRICT>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2, kfull);
+  const int kfull = max_iter - max_iter % KV;
+  int n = vote_loop2_f32<STRICT, KV>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2,
+                                     kfull);
   if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
     for (; n < max_iter; ++n) {
       Iter<float, STRICT>::step(x, y, cr, ci, alive, cnt);
@@ -861,7 +864,7 @@ struct ContQueue {
 // replay per orbit, deferred to the end).
 // PRE > 0: the first PRE iterations run the exact vote loop (counts of the orbits that
 // end there are final); the amortised sub-blocks continue the rest from PRE.
-template <class T, bool STRICT, bool MANDEL, bool COLOR, int KS = 0, int PRE = 0>
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int KS = 0, int PRE = 0, int KV = 4>
 __global__ void __launch_bounds__(kThreads)
 escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, int budget,
                      ContQueue* q, QItem<T>* items) {
@@ -968,7 +971,8 @@ escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
     if (q0) cnt += rc;
     if (q1) cnt2 += rc2;
   } else if constexpr (kAsmPair<T, STRICT, 4>) {
-    vote_loop2_f32<STRICT>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2, budget);
+    vote_loop2_f32<STRICT, KV>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2,
+                               budget);
   } else {
     for (int n = 0; n < budget; n += 4) {
 #pragma unroll

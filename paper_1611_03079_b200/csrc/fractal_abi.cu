@@ -29,6 +29,14 @@ int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
 }
+
+// Vote block of the fast fp32 two-orbit loops in S2 and P1 (FRACTAL_VOTE_K: 4 default,
+// 2 for the same-box A/B of DESIGN.md §5.1b)
+int vote_k() {
+  static const int v = env_int("FRACTAL_VOTE_K", 4);
+  return v == 2 ? 2 : 4;
+}
+
 bool env_is(const char* name, const char* value) {
   const char* e = std::getenv(name);
   return e && !std::strcmp(e, value);
@@ -180,8 +188,11 @@ cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr:
   if constexpr (NC == 1 && std::is_same<T, float>::value) {
     if (s2 && g.counts8 == nullptr) {
       const dim3 grid2 = tile_grid(g, (g.rows + 2 * fr::kTileH - 1) / (2 * fr::kTileH), 1);
-      fr::escape_tile2_kernel<STRICT, MANDEL, COLOR>
-          <<<grid2, fr::kThreads, 0, s>>>(g, pal, cs.re[0], cs.im[0]);
+      auto k2 = fr::escape_tile2_kernel<STRICT, MANDEL, COLOR>;
+      if constexpr (!STRICT) {
+        if (vote_k() == 2) k2 = fr::escape_tile2_kernel<STRICT, MANDEL, COLOR, 2>;
+      }
+      k2<<<grid2, fr::kThreads, 0, s>>>(g, pal, cs.re[0], cs.im[0]);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return cudaGetLastError();
     }
@@ -417,6 +428,9 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   static const int p1ks = env_int("FRACTAL_P1_AMORT", FR_P1A_KS);
   static const int p1pre = env_int("FRACTAL_P1_PRE", FR_P1A_PRE);
   auto kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR>;
+  if constexpr (!STRICT && std::is_same<T, float>::value) {
+    if (vote_k() == 2) kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 0, 0, 2>;
+  }
   if constexpr (!STRICT) {
     if (amort && budget > p1pre && (budget - p1pre) % 8 == 0) {
       if (p1ks == 4 && p1pre == 0) kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 4>;
