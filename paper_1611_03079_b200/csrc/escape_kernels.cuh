@@ -864,15 +864,13 @@ struct ContQueue {
 // replay per orbit, deferred to the end).
 // PRE > 0: the first PRE iterations run the exact vote loop (counts of the orbits that
 // end there are final); the amortised sub-blocks continue the rest from PRE.
-template <class T, bool STRICT, bool MANDEL, bool COLOR, int KS = 0, int PRE = 0, int KV = 4>
-__global__ void __launch_bounds__(kThreads)
-escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, int budget,
-                     ContQueue* q, QItem<T>* items) {
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int KS, int PRE, int KV>
+__device__ __forceinline__ void budget_tile(const Geom& g, const Palette& pal, const T jcr,
+                                            const T jci, int budget, ContQueue* q,
+                                            QItem<T>* items, const int tx, const int ty) {
   // CTA tile 32x16: each thread iterates the pixels of rows ly and ly + 8 of its 8x4-lane
   // warp tile together (two orbits, one vote per block of 4; the S2 layout).  Colours come
   // from the device palette: no CTA barrier in these short-lived CTAs.
-  int tx, ty, grp;
-  tile_of(g, tx, ty, grp);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int px = tx * kTileW + (warp & 3) * kWarpW + (lane & 7);
@@ -1020,6 +1018,21 @@ escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
       items[base + (unsigned)__popc(b0) + (unsigned)__popc(b1 & lt)] = it;
     }
   }
+}
+
+// NT > 1: each CTA renders NT vertically adjacent 32x16 tiles one after the other (fewer,
+// longer CTAs; the FRACTAL_P1_TILES experiment of DESIGN.md §5.1c)
+template <class T, bool STRICT, bool MANDEL, bool COLOR, int KS = 0, int PRE = 0, int KV = 4,
+          int NT = 1>
+__global__ void __launch_bounds__(kThreads)
+escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, int budget,
+                     ContQueue* q, QItem<T>* items) {
+  int tx, ty, grp;
+  tile_of(g, tx, ty, grp);
+#pragma unroll 1
+  for (int h = 0; h < NT; ++h)
+    budget_tile<T, STRICT, MANDEL, COLOR, KS, PRE, KV>(g, pal, jcr, jci, budget, q, items, tx,
+                                                       ty * NT + h);
 }
 
 // AMORT (P2 only, under the escape-monotonicity precondition |C| <= 1.989 checked on the

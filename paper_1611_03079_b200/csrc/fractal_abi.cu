@@ -420,7 +420,10 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   e = buffer_for(g_items, s, (size_t)n * sizeof(fr::QItem<T>), &ip);
   if (e != cudaSuccess) return e;
   auto* items = static_cast<fr::QItem<T>*>(ip);
-  const dim3 grid1 = tile_grid(g, (g.rows + 2 * fr::kTileH - 1) / (2 * fr::kTileH), 1);
+  // FRACTAL_P1_TILES=2: each P1 CTA renders two vertically adjacent tiles (exact P1 only)
+  static const int p1nt = env_int("FRACTAL_P1_TILES", 1) == 2 ? 2 : 1;
+  const dim3 grid1 =
+      tile_grid(g, (g.rows + 2 * p1nt * fr::kTileH - 1) / (2 * p1nt * fr::kTileH), 1);
   const int budget = twophase_budget(amort);
   // amortised P1 under the same precondition as the amortised P2 (FRACTAL_P1_AMORT:
   // 0 = exact test, else sub-blocks of 4 or 8 when the budget is a multiple of it)
@@ -445,6 +448,9 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
         kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 8, 16>;
     }
   }
+  // the two-tile CTA is the exact P1 alone (it overrides the other P1 knobs): its grid
+  // covers half as many tile rows
+  if (p1nt == 2) kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 0, 0, 4, 2>;
   kern1<<<grid1, fr::kThreads, 0, s>>>(g, pal, jcr, jci, budget, q, items);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;

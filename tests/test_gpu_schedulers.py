@@ -20,6 +20,7 @@ SUBSET = ("test_strict_configs_full_frame or test_strict_fuzz or test_strict_rag
                                  {"FRACTAL_SCHED": "twophase", "FRACTAL_BUDGET": "4"},
                                  {"FRACTAL_SCHED": "twophase", "FRACTAL_BUDGET": "48",
                                   "FRACTAL_P2_OCC": "1"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_TILES": "2"},
                                  {"FRACTAL_SCHED": "refill", "FRACTAL_REFILL_CPC": "16"},
                                  {"FRACTAL_SCHED": "amort", "FRACTAL_REFILL_CPC": "0"}])
 def test_parity_under_forced_scheduler(env):
@@ -91,6 +92,7 @@ def test_fast_mode_identical_across_schedulers():
                                  {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_AMORT": "8",
                                   "FRACTAL_P1_PRE": "16"},
                                  {"FRACTAL_VOTE_K": "2"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_TILES": "2"},
                                  {"FRACTAL_SCHED": "refill"}, {"FRACTAL_SCHED": "amort"},
                                  {"FRACTAL_SCHED": "static"}])
 def test_fast_exact_under_forced_scheduler(env):
