@@ -385,9 +385,11 @@ constexpr int64_t kTwoPhaseMaxPixels = int64_t(1) << 25;  // item buffer <= 1 Gi
 // P1's budget (FRACTAL_BUDGET, multiple of 4): 96 before an exact P2, 48 before the
 // amortised P2, whose iterations are cheaper (cfg3 fast, 3 CTAs/SM, K 64: 48/64/96
 // 0.1679/0.1685/0.1719 ms)
-int twophase_budget(bool amort) {
+// fp64 fast with the amortised P1 (below): 64 (cfg3 FP64_FAST, KS 8, prefix 8: budget
+// 32/40/48/64 0.2459/0.2442/0.2443/0.2433 ms; exact P1 at 48 0.2464)
+int twophase_budget(bool amort, bool f64) {
   static const int b = env_int("FRACTAL_BUDGET", 0);
-  const int v = b > 0 ? b : (amort ? 48 : 96);
+  const int v = b > 0 ? b : (amort ? (f64 ? 64 : 48) : 96);
   return v < 4 ? 4 : v - v % 4;
 }
 
@@ -424,12 +426,16 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   static const int p1nt = env_int("FRACTAL_P1_TILES", 1) == 2 ? 2 : 1;
   const dim3 grid1 =
       tile_grid(g, (g.rows + 2 * p1nt * fr::kTileH - 1) / (2 * p1nt * fr::kTileH), 1);
-  const int budget = twophase_budget(amort);
+  const int budget = twophase_budget(amort, sizeof(T) == 8);
   // amortised P1 under the same precondition as the amortised P2 (FRACTAL_P1_AMORT:
   // 0 = exact test, else sub-blocks of 4 or 8 when the budget is a multiple of it)
   // FRACTAL_P1_PRE: exact prefix of 0 / 8 / 16 iterations before the amortised blocks
-  static const int p1ks = env_int("FRACTAL_P1_AMORT", FR_P1A_KS);
-  static const int p1pre = env_int("FRACTAL_P1_PRE", FR_P1A_PRE);
+  // Defaults: exact P1 in fp32 (the amortised one is 3.5% slower there); in fp64 fast
+  // sub-blocks of 8 after an exact prefix of 8 (cfg3 0.2464 -> 0.2433 ms with budget 64)
+  static const int p1ks_env = env_int("FRACTAL_P1_AMORT", -1);
+  static const int p1pre_env = env_int("FRACTAL_P1_PRE", -1);
+  const int p1ks = p1ks_env >= 0 ? p1ks_env : (sizeof(T) == 8 ? 8 : FR_P1A_KS);
+  const int p1pre = p1pre_env >= 0 ? p1pre_env : (sizeof(T) == 8 ? 8 : FR_P1A_PRE);
   auto kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR>;
   if constexpr (!STRICT && std::is_same<T, float>::value) {
     if (vote_k() == 2) kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 0, 0, 2>;
@@ -654,7 +660,8 @@ fr_status render_frame(bool mandel, fr_complex c, fr_window win, int32_t width, 
         e = col ? launch_amort_mode<false, true>(mode, g, p, cc, stream)
                 : launch_amort_mode<false, false>(mode, g, p, cc, stream);
     } else if (sched == kTwoPhase &&
-               max_iter > twophase_budget(p2_amort(mode, mandel, c, win)) &&
+               max_iter > twophase_budget(p2_amort(mode, mandel, c, win),
+                                          mode == FR_FP64_FAST || mode == FR_FP64_STRICT) &&
                (int64_t)g.rows * g.W <= kTwoPhaseMaxPixels) {
       const bool am = p2_amort(mode, mandel, c, win);
       if (mandel)
