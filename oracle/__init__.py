@@ -87,6 +87,10 @@ def _load():
         lib.oracle_escape_fma_f32.restype = i32
         lib.oracle_escape_fma_f64.argtypes = [f64, f64, f64, f64, i32]
         lib.oracle_escape_fma_f64.restype = i32
+        lib.oracle_escape_fma_unscaled_f32.argtypes = [f32, f32, f32, f32, i32]
+        lib.oracle_escape_fma_unscaled_f32.restype = i32
+        lib.oracle_escape_fma_unscaled_f64.argtypes = [f64, f64, f64, f64, i32]
+        lib.oracle_escape_fma_unscaled_f64.restype = i32
         lib.oracle_frame_fma.argtypes = [i32, f64, f64, f64, f64, f64, f64, i64, i64, i32, i32,
                                          vp, i32]
         lib.oracle_frame_fma.restype = i32
@@ -141,6 +145,17 @@ def escape_time(z0: complex, c: complex, max_iter: int = 100, precision=64,
         f = lib.oracle_escape_fma_f32 if _prec(precision) == 32 else lib.oracle_escape_fma_f64
     else:
         f = lib.oracle_escape_f32 if _prec(precision) == 32 else lib.oracle_escape_f64
+    return int(f(z0.real, z0.imag, c.real, c.imag, int(max_iter)))
+
+
+def escape_time_fast_unscaled(z0: complex, c: complex, max_iter: int = 100,
+                              precision=64) -> int:
+    """The unscaled FMA contraction of the strict iteration (yy = y*y; m = fma(x,x,yy);
+    t = fma(x,x,-yy); y = fma(2x,y,ci); x = t + cr): equal to the FAST (doubled-state)
+    sequence unless an unscaled product is subnormal.  For the equivalence pin only."""
+    lib = _load()
+    f = (lib.oracle_escape_fma_unscaled_f32 if _prec(precision) == 32
+         else lib.oracle_escape_fma_unscaled_f64)
     return int(f(z0.real, z0.imag, c.real, c.imag, int(max_iter)))
 
 

@@ -15,7 +15,8 @@
  * Two operation sequences of the same count definition: the strict one
  * (oracle_escape_f32/f64, DESIGN.md §2 / reading c-9) and the FAST one
  * (oracle_escape_fma_f32/f64: explicit C99 fmaf/fma calls, each one correctly
- * rounded fused operation; reading c-10 and its supplement).
+ * rounded fused operation, on the doubled state; reading c-10 and its
+ * supplement).
  */
 #include <float.h>
 #include <math.h>
@@ -119,18 +120,54 @@ int oracle_escape_f64(double zre, double zim, double cre, double cim, int max_it
 
 /* ------------------------------------------------------------------------- */
 /* FAST-mode escape time: the same count definition with the FMA-contracted  */
-/* operation sequence that defines the *_FAST modes (DESIGN.md §5 "State     */
-/* representation", reading c-10; the paper fixes no contraction, so this    */
-/* sequence is the project's definition of FAST, written here in its natural  */
-/* unscaled form with C99's correctly rounded fmaf/fma):                      */
-/*   yy = y*y; m = fma(x, x, yy); if (m > 4) return n;                        */
-/*   t = fma(x, x, -yy); y = fma(x + x, y, ci); x = t + cr;                   */
-/* (x + x is exact.)  Independent of the GPU code, which keeps the state      */
-/* doubled; the two are equal because every step differs by an exact power   */
-/* of two.                                                                    */
+/* operation sequence that DEFINES the *_FAST modes (reading c-10, */
+/* §5 "State representation"; the paper fixes no contraction, so FAST is the */
+/* project's own definition).  The state is kept doubled, X = 2x, Y = 2y,    */
+/* CR = 2cr, CI = 2ci (each doubling exact: no overflow below 2^127), and    */
+/* one iteration is, with C99's correctly rounded fmaf/fma:                   */
+/*   YY = Y*Y; M = fma(X, X, YY); if (M > 16) return n;                       */
+/*   T = fma(X, X, -YY); Y' = fma(X, Y, CI); X' = fma(T, 0.5, CR);             */
+/* This is the FMA contraction of reading c-9's iteration scaled by 2 -- it   */
+/* equals the unscaled contraction below (oracle_escape_fma_unscaled_*)       */
+/* step by step whenever no unscaled product (x*x, y*y, 2x*y) is subnormal,   */
+/* because then every rounding commutes with the power-of-two scaling; where */
+/* one is subnormal the doubled product keeps bits the unscaled one loses     */
+/* (reading c-10, "doubled state").                                 */
 /* ------------------------------------------------------------------------- */
 
 int oracle_escape_fma_f32(float zre, float zim, float cre, float cim, int max_iter) {
+    float X = zre + zre, Y = zim + zim, CR = cre + cre, CI = cim + cim;
+    for (int n = 0; n < max_iter; ++n) {
+        float YY = Y * Y;
+        float M = fmaf(X, X, YY);
+        if (M > 16.0f) return n;
+        float T = fmaf(X, X, -YY);
+        float Yn = fmaf(X, Y, CI);
+        X = fmaf(T, 0.5f, CR);
+        Y = Yn;
+    }
+    return max_iter;
+}
+
+int oracle_escape_fma_f64(double zre, double zim, double cre, double cim, int max_iter) {
+    double X = zre + zre, Y = zim + zim, CR = cre + cre, CI = cim + cim;
+    for (int n = 0; n < max_iter; ++n) {
+        double YY = Y * Y;
+        double M = fma(X, X, YY);
+        if (M > 16.0) return n;
+        double T = fma(X, X, -YY);
+        double Yn = fma(X, Y, CI);
+        X = fma(T, 0.5, CR);
+        Y = Yn;
+    }
+    return max_iter;
+}
+
+/* The unscaled FMA contraction of reading c-9's iteration (for the          */
+/* equivalence pin in tests/test_oracle_fast.py only):                       */
+/*   yy = y*y; m = fma(x, x, yy); if (m > 4) return n;                        */
+/*   t = fma(x, x, -yy); y = fma(x + x, y, ci); x = t + cr;   (x + x exact)   */
+int oracle_escape_fma_unscaled_f32(float zre, float zim, float cre, float cim, int max_iter) {
     float x = zre, y = zim;
     for (int n = 0; n < max_iter; ++n) {
         float yy = y * y;
@@ -144,7 +181,8 @@ int oracle_escape_fma_f32(float zre, float zim, float cre, float cim, int max_it
     return max_iter;
 }
 
-int oracle_escape_fma_f64(double zre, double zim, double cre, double cim, int max_iter) {
+int oracle_escape_fma_unscaled_f64(double zre, double zim, double cre, double cim,
+                                   int max_iter) {
     double x = zre, y = zim;
     for (int n = 0; n < max_iter; ++n) {
         double yy = y * y;

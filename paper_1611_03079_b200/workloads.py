@@ -128,11 +128,16 @@ def palette(name: str = "classic"):
 # ---------------------------------------------------------------- fuzzing
 def fuzz_cases(n: int, max_side: int = 512, seed: int = FUZZ_SEED):
     """Seeded random (C, window, W, H, max_iter) cases: C near the Mandelbrot boundary
-    region |C| <= 1.2, windows of random centre/scale, ragged sizes."""
+    region |C| <= 1.2 for 4 cases in 5, and 1.2 < |C| <= 2.5 for the fifth -- past the
+    escape-monotonicity bound |C| <= 1.989 of the amortised kernels,
+    where an orbit can leave radius 2 and come back -- windows of random centre/scale,
+    ragged sizes."""
     rng = np.random.default_rng(seed)
     out = []
-    for _ in range(n):
+    for k in range(n):
         r = 1.2 * math.sqrt(rng.uniform())
+        if k % 5 == 4:
+            r = float(rng.uniform(1.2, 2.5))
         th = rng.uniform(0, 2 * math.pi)
         c = complex(r * math.cos(th), r * math.sin(th))
         w = int(rng.integers(1, max_side + 1))

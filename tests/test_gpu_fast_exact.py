@@ -2,8 +2,8 @@
 
 FP32_FAST / FP64_FAST are defined (DESIGN.md §5 "State representation", reading c-10)
 as the escape-time iteration carried out with one FMA-contracted operation sequence;
-oracle/escape_oracle.c's oracle_escape_fma_* writes that sequence in its unscaled
-form with C99 fmaf/fma, independent of the kernels (which keep the state doubled).
+oracle/escape_oracle.c's oracle_escape_fma_* writes that sequence (doubled state,
+C99 fmaf/fma) plainly, independent of the kernels.
 Because both are the same sequence of correctly rounded operations, the counts must
 agree exactly -- a stronger check than the tolerance test_gpu_parity.py applies
 against the strict oracle, which stays as the statement of how far FAST is from the
@@ -154,3 +154,27 @@ def test_fast_cfg5_sampled(fr):
     np.testing.assert_array_equal(sample16(got, py, px), ref)
     del got
     torch.cuda.empty_cache()
+
+
+NONMONO_C = (-2 + 0j, -2.1 + 0j, 2j, -5 + 0j, 3 + 1j, 1.995 + 0j, -1.4 - 1.4j)
+
+
+@pytest.mark.parametrize("c", NONMONO_C)
+@pytest.mark.parametrize("mi", [100, 300, 1000])
+def test_fast_nonmonotone_julia(fr, c, mi):
+    """|C| > 1.989 (no escape monotonicity): FAST counts equal the FAST oracle whatever
+    kernel the host routes to (the amortised ones must not be used here)."""
+    w, h = 241, 161
+    win = W.Window(0j, 2.6, 2.6 * h / w)
+    for prec in (32, 64):
+        ref = oracle.julia(c, win.center, win.half_w, win.half_h, w, h, mi, prec, fast=True)
+        np.testing.assert_array_equal(gpu_julia(fr, c, win, w, h, mi, fast(prec, fr)), ref)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_fast_nonmonotone_mandelbrot_window(fr, prec):
+    """A Mandelbrot window reaching |c| = 2.6 (corners outside the monotone bound)."""
+    win = W.Window(-0.3 + 0.1j, 2.3, 1.4)
+    for mi in (100, 1000):
+        ref = oracle.mandelbrot(win.center, win.half_w, win.half_h, 301, 183, mi, prec, fast=True)
+        np.testing.assert_array_equal(gpu_mandel(fr, win, 301, 183, mi, fast(prec, fr)), ref)

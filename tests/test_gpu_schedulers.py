@@ -12,7 +12,8 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 SUBSET = ("test_strict_configs_full_frame or test_strict_fuzz or test_strict_ragged or "
-          "test_bands or test_max_iter_65535 or test_every_pixel or test_fast_mode_tolerance_julia")
+          "test_bands or test_max_iter_65535 or test_every_pixel or test_fast_mode_tolerance_julia "
+          "or test_nonmonotone")
 
 
 @pytest.mark.parametrize("env", [{"FRACTAL_SCHED": "static"}, {"FRACTAL_SCHED": "refill"},
@@ -105,7 +106,7 @@ def test_fast_exact_under_forced_scheduler(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-m", "pytest",
                         os.path.join(ROOT, "tests", "test_gpu_fast_exact.py"), "-m", "gpu", "-q",
-                        "-x", "-k", "fast_configs or fast_fuzz or fast_mandelbrot",
+                        "-x", "-k", "fast_configs or fast_fuzz or fast_mandelbrot or fast_nonmonotone",
                         "-p", "no:cacheprovider"],
                        cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

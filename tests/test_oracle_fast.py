@@ -1,5 +1,6 @@
-"""Pins for the FAST-mode oracle (oracle_escape_fma_*: the FMA-contracted sequence that
-defines FP32_FAST / FP64_FAST, DESIGN.md §5 "State representation", reading c-10).
+"""Pins for the FAST-mode oracle (oracle_escape_fma_*: the FMA-contracted sequence on the
+doubled state X = 2x, Y = 2y that defines FP32_FAST / FP64_FAST, DESIGN.md §5 "State
+representation", reading c-10).
 
 What fixes it, independent of its own code:
   * exact dyadic orbits: every operation is exact, so fused and unfused agree and the
@@ -9,7 +10,9 @@ What fixes it, independent of its own code:
     segment, the Mandelbrot regions, the 180-degree / conjugate symmetries (fma and
     round-to-nearest are sign-symmetric), cap monotonicity;
   * a brute force in exact rational arithmetic with its own round-to-nearest-even to
-    binary32 / binary64 (no libm fma), on tiny grids;
+    binary32 / binary64 (no libm fma), on tiny grids, of BOTH the doubled sequence (the
+    definition) and the unscaled contraction of reading c-9's iteration (the doubled one
+    is its exact power-of-two rescaling while no unscaled product is subnormal);
   * that the sequence is really fused: on a 1080p-shaped frame it differs from the
     strict oracle on a small, nonzero fraction of pixels.
 """
@@ -139,6 +142,64 @@ def _brute_fast(z0: complex, c: complex, mi: int, prec: int) -> int:
         t = R(x * x - yy)            # fused
         x, y = R(t + cr), R(2 * x * y + ci)  # y: fused 2x*y + ci
     return mi
+
+
+def _brute_fast_doubled(z0: complex, c: complex, mi: int, prec: int) -> int:
+    """The FAST definition as written (doubled state): YY = Y*Y; M = fma(X,X,YY) > 16?;
+    T = fma(X,X,-YY); Y' = fma(X,Y,CI); X' = fma(T,1/2,CR), every fused op rounded once."""
+    R = lambda v: _rn(v, prec)  # noqa: E731
+    X, Y = 2 * R(Fraction(z0.real)), 2 * R(Fraction(z0.imag))
+    CR, CI = 2 * R(Fraction(c.real)), 2 * R(Fraction(c.imag))
+    for n in range(mi):
+        YY = R(Y * Y)
+        if R(X * X + YY) > 16:
+            return n
+        T = R(X * X - YY)
+        X, Y = R(T / 2 + CR), R(X * Y + CI)
+    return mi
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_fast_oracle_matches_doubled_brute_force(oracle_mod, prec):
+    """The definition itself: the oracle's doubled FMA sequence against an exact-rational
+    evaluation of the same sequence with its own rounding, on tiny fuzz grids."""
+    for c, win, w, h, mi in W.fuzz_cases(5, max_side=9, seed=12):
+        mi = min(mi, 120)
+        g = oracle.julia(c, win.center, win.half_w, win.half_h, w, h, mi, prec, fast=True)
+        m = oracle.mandelbrot(win.center, win.half_w, win.half_h, w, h, mi, prec, fast=True)
+        for py in range(h):
+            for px in range(w):
+                z = oracle.pixel_to_complex(win.center, win.half_w, win.half_h, w, h, px, py)
+                if prec == 32:
+                    z = complex(np.float32(z.real), np.float32(z.imag))
+                assert g[py, px] == _brute_fast_doubled(z, c, mi, prec), (c, px, py)
+                assert m[py, px] == _brute_fast_doubled(0j, z, mi, prec), (z, px, py)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_doubled_equals_unscaled_contraction(oracle_mod, prec):
+    """Away from subnormal products the doubled FAST sequence is the unscaled FMA
+    contraction of reading c-9's iteration rescaled by 2 (every rounding commutes with
+    the scaling): the two oracle functions agree orbit for orbit on fuzz starts, and on
+    a 1080p-shaped frame's worth of sampled pixels."""
+    rng = np.random.default_rng(77)
+    for _ in range(3000):
+        z0 = complex(*rng.uniform(-2.2, 2.2, 2))
+        c = complex(*rng.uniform(-1.5, 1.5, 2))
+        mi = int(rng.choice([7, 100, 1000]))
+        assert (oracle.escape_time(z0, c, mi, prec, fast=True)
+                == oracle.escape_time_fast_unscaled(z0, c, mi, prec)), (z0, c, mi)
+
+
+def test_doubled_differs_only_through_subnormals():
+    """Where an unscaled product is subnormal the doubled one keeps bits: y = 3 * 2^-75 in
+    binary32 has y*y = 4.5 subnormal quanta (2^-149), rounded to 4, while 4y^2 = 18
+    quanta is exact, so fl(4 y^2) != 4 fl(y^2) (reading c-10's stated exception to the
+    equivalence above)."""
+    y = Fraction(3, 2 ** 75)
+    assert _rn(4 * y * y, 32) != 4 * _rn(y * y, 32)
+    y = Fraction(3, 2 ** 40)  # normal range: the scaling commutes
+    assert _rn(4 * y * y, 32) == 4 * _rn(y * y, 32)
 
 
 @pytest.mark.parametrize("prec", PRECS)

@@ -391,3 +391,34 @@ def test_nudged_pixels(oracle_mod):
         assert (a != c).sum() < 0.1 * a.size
         if prec == 32:
             assert (a != c).sum() > 0
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("kind", ["julia", "mandelbrot"])
+@pytest.mark.parametrize("nudge", [1, 3])
+def test_nudge_is_exactly_n_ulps(oracle_mod, prec, kind, nudge):
+    """The nudge of reading c-10's sensitivity bound moves the start value's real part
+    (Julia Z_0, Mandelbrot C) by exactly `nudge` ulps of the working precision toward
+    +inf: each sampled count equals the plain escape time of the start value stepped
+    with numpy's nextafter, pixel by pixel (a 4-ulp nudge in place of 1 would fail)."""
+    rng = np.random.default_rng(8)
+    w, h, mi = 320, 180, 1000
+    px, py = rng.integers(0, w, 300), rng.integers(0, h, 300)
+    c = -0.7269 + 0.1889j
+    center, hw, hh = (0j, 2.0, 1.125) if kind == "julia" else (-0.5 + 0j, 1.5, 0.85)
+    got = oracle.pixels_nudged(kind, c, center, hw, hh, w, h, mi, prec, px, py, nudge)
+    dt = np.float32 if prec == 32 else np.float64
+    differs = 0
+    for k in range(px.size):
+        z = oracle.pixel_to_complex(center, hw, hh, w, h, int(px[k]), int(py[k]))
+        re = dt(z.real)
+        for _ in range(nudge):
+            re = np.nextafter(re, dt(np.inf))
+        start = complex(float(re), float(dt(z.imag)))
+        want = (oracle.escape_time(start, c, mi, prec) if kind == "julia"
+                else oracle.escape_time(0j, start, mi, prec))
+        assert got[k] == want, (kind, px[k], py[k])
+        differs += int(want != oracle.escape_time(z if kind == "julia" else 0j,
+                                                  c if kind == "julia" else z, mi, prec))
+    if prec == 32:
+        assert differs > 0  # the nudge is not a no-op at this sensitivity
