@@ -433,11 +433,95 @@ __device__ __forceinline__ int fast_vote_loop_f32<4>(float& x, float& y, int& cn
   "fma.rn.f32 %0, t, 0f3F000000, %12;\n\t"           \
   "fma.rn.f32 %5, t2, 0f3F000000, %14;\n\t"
 
+// Packed form (sm_100 FFMA2 / FMUL2): the two orbits are the two halves of 64-bit
+// register pairs X = (x, x2), Y = (y, y2), CR = (cr, crb), CI = (ci, cib); one packed
+// instruction runs the same correctly rounded fused operation on both halves, so the
+// counts are bit-identical to the scalar loop.  The packed FP instructions keep the FMA
+// pipe busy two cycles each while the escape tests (FSETP) and predicated count
+// increments issue in between: 5 packed + 4 scalar + 1/K vote issue slots per pair of
+// pixel-iterations instead of 10 + 4 (microbenchmark: 1.33x, profiles/r02/).
+// -YY is formed by unpack + neg + repack, which ptxas folds into an FFMA2 operand
+// modifier (no instruction).
+#define FR_FAST_STEP2X                               \
+  "mul.rn.f32x2 yy, Y, Y;\n\t"                       \
+  "fma.rn.f32x2 m, X, X, yy;\n\t"                    \
+  "mov.b64 {m1, m2}, m;\n\t"                         \
+  "setp.le.and.f32 pa, m1, 0f41800000, pa;\n\t"      \
+  "setp.le.and.f32 pb, m2, 0f41800000, pb;\n\t"      \
+  "@pa add.s32 %2, %2, 1;\n\t"                       \
+  "@pb add.s32 %7, %7, 1;\n\t"                       \
+  "mov.b64 {n1, n2}, yy;\n\t"                        \
+  "neg.f32 n1, n1;\n\t"                              \
+  "neg.f32 n2, n2;\n\t"                              \
+  "mov.b64 nyy, {n1, n2};\n\t"                       \
+  "fma.rn.f32x2 t, X, X, nyy;\n\t"                   \
+  "fma.rn.f32x2 Y, X, Y, CI;\n\t"                    \
+  "fma.rn.f32x2 X, t, HALF, CR;\n\t"
+
+#ifndef FR_FFMA2
+#define FR_FFMA2 1  // 0: the scalar two-orbit loop (same-box A/B)
+#endif
+
 template <int K>
 __device__ __forceinline__ int fast_vote_loop2_f32(float& x, float& y, int& cnt, unsigned& alive,
                                                    float& x2, float& y2, int& cnt2,
                                                    unsigned& alive2, float cr2, float ci2,
                                                    float cr2b, float ci2b, int kfull);
+
+template <int K>
+__device__ __forceinline__ int fast_vote_loop2x_f32(float& x, float& y, int& cnt,
+                                                    unsigned& alive, float& x2, float& y2,
+                                                    int& cnt2, unsigned& alive2, float cr2,
+                                                    float ci2, float cr2b, float ci2b,
+                                                    int kfull) {
+  static_assert(K == 2 || K == 4, "vote blocks of 2 or 4");
+  int n;
+  if constexpr (K == 4) {
+    asm volatile(
+        "{\n\t.reg .pred pa, pb, pm;\n\t.reg .b64 X, Y, CR, CI, HALF, yy, m, nyy, t;\n\t"
+        ".reg .f32 m1, m2, n1, n2;\n\t"
+        "mov.b64 X, {%0, %5};\n\tmov.b64 Y, {%1, %6};\n\t"
+        "mov.b64 CR, {%12, %14};\n\tmov.b64 CI, {%13, %15};\n\t"
+        "mov.b64 HALF, {0f3F000000, 0f3F000000};\n\t"
+        "setp.ne.u32 pa, %3, 0;\n\tsetp.ne.u32 pb, %8, 0;\n\tmov.u32 %4, 0;\n\t"
+        "setp.gt.s32 pm, %9, 0;\n\t@!pm bra FR_X4B_DONE;\n"
+        "FR_X4B_LOOP:\n\t" FR_FAST_STEP2X FR_FAST_STEP2X FR_FAST_STEP2X FR_FAST_STEP2X
+        "add.s32 %4, %4, 4;\n\t"
+        "or.pred pm, pa, pb;\n\t"
+        "vote.sync.any.pred pm, pm, 0xffffffff;\n\t"
+        "setp.lt.and.s32 pm, %4, %9, pm;\n\t"
+        "@pm bra FR_X4B_LOOP;\n"
+        "FR_X4B_DONE:\n\t"
+        "mov.b64 {%0, %5}, X;\n\tmov.b64 {%1, %6}, Y;\n\t"
+        "selp.u32 %3, 1, 0, pa;\n\tselp.u32 %8, 1, 0, pb;\n\t}"
+        : "+f"(x), "+f"(y), "+r"(cnt), "+r"(alive), "=r"(n), "+f"(x2), "+f"(y2), "+r"(cnt2),
+          "+r"(alive2)
+        : "r"(kfull), "r"(0), "r"(0), "f"(cr2), "f"(ci2), "f"(cr2b), "f"(ci2b));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred pa, pb, pm;\n\t.reg .b64 X, Y, CR, CI, HALF, yy, m, nyy, t;\n\t"
+        ".reg .f32 m1, m2, n1, n2;\n\t"
+        "mov.b64 X, {%0, %5};\n\tmov.b64 Y, {%1, %6};\n\t"
+        "mov.b64 CR, {%12, %14};\n\tmov.b64 CI, {%13, %15};\n\t"
+        "mov.b64 HALF, {0f3F000000, 0f3F000000};\n\t"
+        "setp.ne.u32 pa, %3, 0;\n\tsetp.ne.u32 pb, %8, 0;\n\tmov.u32 %4, 0;\n\t"
+        "setp.gt.s32 pm, %9, 0;\n\t@!pm bra FR_X2B_DONE;\n"
+        "FR_X2B_LOOP:\n\t" FR_FAST_STEP2X FR_FAST_STEP2X
+        "add.s32 %4, %4, 2;\n\t"
+        "or.pred pm, pa, pb;\n\t"
+        "vote.sync.any.pred pm, pm, 0xffffffff;\n\t"
+        "setp.lt.and.s32 pm, %4, %9, pm;\n\t"
+        "@pm bra FR_X2B_LOOP;\n"
+        "FR_X2B_DONE:\n\t"
+        "mov.b64 {%0, %5}, X;\n\tmov.b64 {%1, %6}, Y;\n\t"
+        "selp.u32 %3, 1, 0, pa;\n\tselp.u32 %8, 1, 0, pb;\n\t}"
+        : "+f"(x), "+f"(y), "+r"(cnt), "+r"(alive), "=r"(n), "+f"(x2), "+f"(y2), "+r"(cnt2),
+          "+r"(alive2)
+        : "r"(kfull), "r"(0), "r"(0), "f"(cr2), "f"(ci2), "f"(cr2b), "f"(ci2b));
+  }
+  return n;
+}
+#undef FR_FAST_STEP2X
 
 template <>
 __device__ __forceinline__ int fast_vote_loop2_f32<4>(float& x, float& y, int& cnt,
@@ -548,7 +632,10 @@ __device__ __forceinline__ int vote_loop2_f32(float& x, float& y, int& cnt, unsi
   if constexpr (STRICT)
     return strict_vote_loop2_f32(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, crb, cib, kfull);
   else
-    return fast_vote_loop2_f32<KV>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, crb, cib, kfull);
+    return FR_FFMA2 ? fast_vote_loop2x_f32<KV>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, crb,
+                                               cib, kfull)
+                    : fast_vote_loop2_f32<KV>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, crb,
+                                              cib, kfull);
 }
 
 #undef FR_FAST_STEP2
@@ -654,11 +741,11 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
                                   __shfl_sync(kFull, cs.re[f + 1], lane),
                                   __shfl_sync(kFull, cs.im[f + 1], lane), kfull);
       else
-        n = fast_vote_loop2_f32<K>(x, y, cnt, alive, x2, y2, cnt2, alive2,
-                                   __shfl_sync(kFull, cs.re[f], lane),
-                                   __shfl_sync(kFull, cs.im[f], lane),
-                                   __shfl_sync(kFull, cs.re[f + 1], lane),
-                                   __shfl_sync(kFull, cs.im[f + 1], lane), kfull);
+        n = vote_loop2_f32<false, K>(x, y, cnt, alive, x2, y2, cnt2, alive2,
+                                     __shfl_sync(kFull, cs.re[f], lane),
+                                     __shfl_sync(kFull, cs.im[f], lane),
+                                     __shfl_sync(kFull, cs.re[f + 1], lane),
+                                     __shfl_sync(kFull, cs.im[f + 1], lane), kfull);
       if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
         for (; n < max_iter; ++n) {
           Iter<T, STRICT>::step(x, y, cs.re[f], cs.im[f], alive, cnt);

@@ -65,4 +65,47 @@ def test_half_stays_an_immediate(sass):
     for name in fast:
         remat = [i for i in funcs[name] if re.search(r"MOV.*0x3f000000", i)]
         assert not remat, (name, remat[:3])
-        assert any(re.search(r"FFMA .*, 0\.5, ", i) for i in funcs[name]), name
+        assert any(re.search(r"FFMA2? .*, 0\.5, ", i) for i in funcs[name]), name
+
+
+def _tile_fn_param(name):
+    """FN template argument of escape_tile_kernel<T, STRICT, MANDEL, COLOR, K, NC, FN, ES>
+    (the Figure 4 map variants; FN = 2 divides)."""
+    m = re.search(r"escape_tile_kernelI[fd](?:Lb[01]E){3}Li(\d+)ELi(\d+)ELi(\d+)E", name)
+    return int(m.group(3)) if m else 0
+
+
+def _strict(name):
+    return (re.search(r"escape_(tile|refill|budget|cont)_kernelI[fd]Lb1E", name) is not None
+            or "escape_tile2_kernelILb1E" in name)
+
+
+def test_strict_kernels_never_fuse(sass):
+    """Reading c-9: STRICT runs every multiply and add separately rounded.  ptxas may
+    contract separately written packed or scalar .rn ops (it does so for mul.rn.f32x2 +
+    add.rn.f32x2), so the strict kernels are checked for fused instructions: none, except
+    in the map variant with the rational term (FN = 2), whose correctly rounded division
+    routine uses FMAs internally.  (HFMA2 -RZ, RZ is ptxas's register-zeroing idiom, not
+    arithmetic, and fp16 is not used.)"""
+    _, funcs = sass
+    strict = [n for n in funcs if _strict(n)]
+    assert len(strict) >= 10
+    for name in strict:
+        if _tile_fn_param(name) == 2:
+            continue
+        fused = [i for i in funcs[name] if re.search(r"\b(FFMA2?|DFMA)\b", i)]
+        assert not fused, (name, fused[:3])
+
+
+def test_fast_two_orbit_loops_are_packed(sass):
+    """The two-orbit fast fp32 vote loops (S frame pairs, S2, exact P1) run on packed
+    FFMA2 / FMUL2 (sm_100): both orbits per instruction."""
+    _, funcs = sass
+    names = [n for n in funcs
+             if "escape_tile2_kernelILb0E" in n
+             or re.search(r"escape_budget_kernelIfLb0ELb[01]ELb[01]ELi0ELi0E", n)
+             or re.search(r"escape_tile_kernelIfLb0ELb0ELb[01]ELi4ELi1024E", n)]
+    assert len(names) >= 6
+    for name in names:
+        assert sum("FFMA2" in i for i in funcs[name]) >= 8, name
+        assert any("FMUL2" in i for i in funcs[name]), name
