@@ -221,6 +221,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extra", action="store_true", help="skip the per-config extras")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--force-exchange", action="store_true",
+                    help="run the N > 1 exchange measurements (gather, pipelined delivery, "
+                         "row bands) even at N = 1, over an NCCL group of one")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
@@ -229,7 +232,13 @@ def main():
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
-    if world > 1:
+    exchange = world > 1 or args.force_exchange
+    if exchange:
+        if world == 1:  # a process group of one (no torchrun): local rendezvous
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1611_03079_b200 import binding as fr
     from paper_1611_03079_b200 import workloads as W
@@ -328,11 +337,12 @@ def main():
         }
     # ---- the exchange step (N > 1): NCCL gather of every rank's frames to rank 0, plain
     # (after the render) and pipelined with the render (chunked, separate stream)
-    gather = measure_gather(out, world, rank, barrier) if world > 1 else None
+    gather = measure_gather(out, world, rank, barrier) if exchange else None
     delivered = (measure_delivered(win, world, rank, barrier, job_iters / args.steps)
-                 if world > 1 else None)
+                 if exchange else None)
     # ---- row bands over the ranks (cfg3 and cfg5 as cyclic bands)
-    bands = measure_bands(world, rank, barrier) if world > 1 and not args.no_extra else None
+    bands = (measure_bands(world, rank, barrier)
+             if exchange and (not args.no_extra or args.force_exchange) else None)
     # ---- end-to-end through the public API with HOST buffers (pinned), N GPUs
     e2e = measure_e2e(fr, W, cs, win, world, args, barrier, stream)
     if rank == 0:
@@ -348,7 +358,7 @@ def main():
             if not args.no_extra:
                 line["configs"] = extras(fr, W, torch)
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if exchange:
         dist.barrier()
         dist.destroy_process_group()
     return 0
@@ -421,10 +431,11 @@ def measure_delivered(win, world, rank, barrier, job_iters_per_step, chunk=64):
 
 
 def measure_bands(world, rank, barrier):
-    """cfg3 (4K Julia, mi 1000, fp32 fast) and cfg5 (16384^2 Mandelbrot, mi 10000, fp64
-    fast) as cyclic row bands over the ranks (band_rows 15 and 16): the compute makespan
-    (max over ranks of each rank's render) and the NCCL gather of the bands to rank 0
-    (distributed.gather_bands), timed separately with CUDA events."""
+    """cfg3 (4K Julia, mi 1000, fp32 fast, fused colour levels) and cfg5 (16384^2
+    Mandelbrot, mi 10000, fp64 fast) as cyclic row bands over the ranks (band_rows 15
+    and 16): the compute makespan (max over ranks of each rank's render) and the NCCL
+    gather of the bands to rank 0 (distributed.gather_bands; cfg3: counts and RGBA),
+    timed separately with CUDA events."""
     import torch
     import torch.distributed as dist
     from paper_1611_03079_b200 import binding as fr
@@ -434,20 +445,28 @@ def measure_bands(world, rank, barrier):
     for name, reps in (("cfg3", 20), ("cfg5", 1)):
         try:
             c = W.configs()[name]
+            pal = W.palette("classic") if c.colorize else None
             if c.kind == "julia":
                 mode = fr.Mode.FP32_FAST
 
                 def render():
                     return D.render_bands("julia", c.window, c.width, c.height, c.max_iter,
-                                          c.band_rows, c=c.c, mode=mode, gather=False)
+                                          c.band_rows, c=c.c, mode=mode, gather=False,
+                                          palette=pal)
             else:
                 mode = fr.Mode.FP64_FAST
 
                 def render():
                     return D.render_bands("mandelbrot", c.window, c.width, c.height,
                                           c.max_iter, c.band_rows, mode=mode, gather=False)
+            def gather(loc):
+                if pal is None:
+                    return D.gather_bands(loc, c.height, c.band_rows)
+                return (D.gather_bands(loc[0], c.height, c.band_rows),
+                        D.gather_bands(loc[1], c.height, c.band_rows))
+
             local = render()  # warm-up (workspaces, survivor buffer, NCCL set-up)
-            _ = D.gather_bands(local, c.height, c.band_rows)
+            _ = gather(local)
             del _
             barrier()
             t0 = torch.cuda.Event(enable_timing=True)
@@ -458,11 +477,12 @@ def measure_bands(world, rank, barrier):
             t1.record()
             barrier()
             ms = t0.elapsed_time(t1) / reps
-            iters = float((local.view(torch.int16).to(torch.int64) & 0xFFFF).sum().item())
+            cnt = local[0] if pal is not None else local
+            iters = float((cnt.view(torch.int16).to(torch.int64) & 0xFFFF).sum().item())
             g0 = torch.cuda.Event(enable_timing=True)
             g1 = torch.cuda.Event(enable_timing=True)
             g0.record()
-            full = D.gather_bands(local, c.height, c.band_rows)
+            full = gather(local)
             g1.record()
             barrier()
             gms = g0.elapsed_time(g1)
@@ -475,8 +495,11 @@ def measure_bands(world, rank, barrier):
             out[name] = {"compute_ms": float(mx[0]), "gather_ms": float(mx[1]),
                          "gpix_iter_s": float(sm[2]) / (float(mx[0]) * 1e-3) / 1e9,
                          "band_rows": c.band_rows, "mode": mode.name,
+                         "colour": "fused classic palette" if pal is not None else None,
+                         "world": world,
                          "note": "cyclic bands, compute makespan = max over ranks; gather "
-                                 "of the uint16 bands to rank 0 (NCCL) timed separately"}
+                                 "of the bands to rank 0 (NCCL; uint16 counts, plus RGBA "
+                                 "when coloured) timed separately"}
         except Exception as e:  # report, never fail the bench line
             out[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
     return out

@@ -37,17 +37,29 @@
  *           heavy-tailed two-phase path (one 16-B item per pixel, 24 B in fp64,
  *           grown on demand, frames up to 2^25 pixels) and, per device, a 1-KB
  *           device copy of each distinct palette.  They are created
- *           on first use and live until process exit; creation is synchronous and
- *           is not allowed inside CUDA graph capture (cudaErrorStreamCaptureUnsupported
+ *           on first use (zeroed / uploaded in stream order on `stream`, which the
+ *           call then synchronises once) and live until process exit; a buffer that
+ *           has to grow is replaced, and the outgrown one is kept alive too, so a CUDA
+ *           graph captured earlier never sees its memory freed.  Creation is not
+ *           allowed inside CUDA graph capture (cudaErrorStreamCaptureUnsupported
  *           -> FR_ERR_CUDA), so make the first call of a kind on a stream outside
  *           capture.
+ *  Graphs.  A captured graph uses the workspaces of the stream it was captured on.
+ *           Replays of such graphs must be stream-ordered with each other and with
+ *           eager calls on that stream (replay on the capture stream, or order the
+ *           replay stream after it with events): the self-resetting counters of two
+ *           overlapping launches sharing one workspace would race.
  *  Async.   Calls validate synchronously, enqueue on `stream` and return.  Outputs
  *           are valid once the caller synchronises the stream; device faults surface
- *           there.  On any error status nothing has been launched.  No C++ exception
- *           crosses the ABI.  Calls are reentrant and thread-safe (the caches above
- *           are mutex-guarded; calls on one stream share its workspaces in stream
- *           order); apart from those caches the library holds only a monotonic
- *           launch counter (fr_launch_count).
+ *           there.  On FR_ERR_INVALID_ARG / FR_ERR_TOO_LARGE / FR_ERR_UNSUPPORTED
+ *           nothing has been launched.  On FR_ERR_CUDA (a failed launch or
+ *           allocation) earlier kernels of the same call -- earlier chunks of a path,
+ *           the first phase of a two-phase frame -- may already be enqueued: the
+ *           output buffers are then undefined.  No C++ exception crosses the ABI.
+ *           Calls are reentrant and thread-safe (the caches above are mutex-guarded;
+ *           calls on one stream share its workspaces in stream order); apart from
+ *           those caches the library holds only a monotonic launch counter
+ *           (fr_launch_count).
  *  Stream.  `stream` is a cudaStream_t (NULL = legacy default stream).
  */
 #ifndef FRACTAL_H_

@@ -186,12 +186,16 @@ _PAL_CACHE = {}
 
 
 def _pal(palette):
-    """Host palette struct, cached per (entries, interior) object pair."""
-    key = (id(palette[0]), id(palette[1]))
+    """Host palette struct, cached by the palette's CONTENT (entries and interior bytes),
+    so a palette edited in place is never served stale."""
+    entries, interior = palette
+    ent = np.ascontiguousarray(np.asarray(entries, dtype=np.uint8).reshape(-1, 4))
+    inter = np.ascontiguousarray(np.asarray(interior, dtype=np.uint8).reshape(4))
+    key = ent.tobytes() + inter.tobytes()
     hit = _PAL_CACHE.get(key)
-    if hit is not None and hit.src[0] is palette[0] and hit.src[1] is palette[1]:
+    if hit is not None:
         return hit
-    h = _PalHolder(palette)
+    h = _PalHolder(ent, inter)
     if len(_PAL_CACHE) > 64:
         _PAL_CACHE.clear()
     _PAL_CACHE[key] = h
@@ -201,11 +205,8 @@ def _pal(palette):
 class _PalHolder:
     """Keeps the host palette buffer alive for the duration of a call."""
 
-    def __init__(self, palette):
-        self.src = palette
-        entries, interior = palette
-        ent = np.ascontiguousarray(np.asarray(entries, dtype=np.uint8).reshape(-1, 4))
-        inter = np.asarray(interior, dtype=np.uint8).reshape(4)
+    def __init__(self, ent, inter):
+        ent = ent.copy()  # owned: the caller may edit its arrays after the call
         self.buf = ent
         self.c = _Palette(ent.ctypes.data, ent.shape[0], (ctypes.c_uint8 * 4)(*inter.tolist()))
 

@@ -1350,6 +1350,220 @@ escape_cont_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Co
 }
 
 // ----------------------------------------------------------------------------------
+// P2 for FP32_FAST under the escape-monotonicity precondition (|C| <= 1.989, host-
+// checked), packed: "P2X" (escape_cont2_kernel) + "P3" (replay_kernel).
+//
+// Each lane runs TWO orbits ("slots" a and b) as the halves of packed float2 registers,
+// so every iteration is 4 FFMA2/FMUL2 for both (the FMA pipe is the bound; the block-end
+// bookkeeping issues on the ALU pipe in between).  Blocks of K bare iterations end with
+// one |Z|^2 test per slot; a finished slot
+//   * (limit reached, end state inside) stores count = max_iter directly: by
+//     monotonicity no earlier state escaped;
+//   * (end state escaped) writes a replay record -- the block's start state and its
+//     iteration index -- over its own (already consumed) queue item, and the exact
+//     escape index is recovered later by P3, one record per thread (SIMT-efficient),
+//     instead of stalling the warp here;
+// and immediately takes the next item from a per-warp ring of queue items in shared
+// memory (refilled 32 items per atomic, so a finished slot never waits for a warp-wide
+// service threshold).  Lanes idle only once the queue is dry.
+// Counts are bit-identical to the FAST oracle: the same doubled FMA sequence (packed
+// halves are separately rounded fused operations), and P3 replays with the
+// per-iteration test of that sequence.
+// ----------------------------------------------------------------------------------
+constexpr int kRing = 128;  // queue items buffered per warp (shared memory; <= 96 live)
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fneg2(float2 a) { return make_float2(-a.x, -a.y); }
+
+template <bool MANDEL, bool COLOR, int K>
+__global__ void __launch_bounds__(kThreads)
+escape_cont2_kernel(const Geom g, const Palette pal, const float jcr2, const float jci2,
+                    ContQueue* q, QItem<float>* items) {
+  __shared__ QItem<float> ring[kThreads / 32][kRing];
+  __shared__ unsigned ringq[kThreads / 32][kRing];  // queue position of each ring entry
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int max_iter = g.max_iter;
+  const unsigned n_items = *reinterpret_cast<volatile unsigned*>(&q->tail);
+  unsigned long long* trace = g_refill_trace;
+  const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + warp;
+  if (trace && lane == 0) trace[gw * 3] = global_ns();
+  QItem<float>* rg = ring[warp];
+  unsigned* rq = ringq[warp];
+  unsigned rhead = 0u, rcount = 0u;  // warp-uniform ring state
+  bool exhausted = false;
+  // refill: append one grab of up to 32 items to the ring (warp-collective)
+  auto refill = [&]() {
+    unsigned base = 0u;
+    if (lane == 0) base = atomicAdd(&q->head, 32u);
+    base = __shfl_sync(kFull, base, 0);
+    if (base >= n_items) {
+      exhausted = true;
+      if (trace && lane == 0) trace[gw * 3 + 1] = global_ns();
+      return;
+    }
+    const unsigned i = base + (unsigned)lane;
+    const unsigned slot = (rhead + rcount + (unsigned)lane) & (kRing - 1);
+    if (i < n_items) {
+      rg[slot] = items[i];
+      rq[slot] = i;
+    }
+    const unsigned got = min(32u, n_items - base);
+    rcount += got;
+    __syncwarp();
+  };
+
+  // slot state: .x = slot a, .y = slot b
+  float2 X = make_float2(0.f, 0.f), Y = X;
+  float2 CR = make_float2(jcr2, jcr2), CI = make_float2(jci2, jci2);
+  int ca = 0, cb = 0;           // iterations done before the current block
+  unsigned ia = 0u, ib = 0u;    // pixel index
+  unsigned qa = 0u, qb = 0u;    // queue position (replay record slot)
+  bool ha = false, hb = false;  // slot holds an orbit
+  auto take = [&](unsigned r, float& x, float& y, float& cr, float& ci, int& c, unsigned& idx,
+                  unsigned& qp) {
+    const unsigned s = (rhead + r) & (kRing - 1);
+    const QItem<float> it = rg[s];
+    x = it.x;
+    y = it.y;
+    c = it.cnt;
+    idx = it.idx;
+    qp = rq[s];
+    if (MANDEL) {
+      const int row = (int)(idx / (unsigned)g.W);
+      const int px = (int)(idx - (unsigned)row * (unsigned)g.W);
+      cr = to_state<float, false>(pixel_re(g, px));
+      ci = to_state<float, false>(pixel_im(g, global_row(g, row)));
+    }
+  };
+  // finished slot: interior (store) or replay record (over its consumed queue item)
+  auto finish = [&](bool esc, float x0, float y0, int c, unsigned idx, unsigned qp) {
+    if (esc) {
+      QItem<float> r;
+      r.x = x0;
+      r.y = y0;
+      r.cnt = c;
+      r.idx = idx;
+      items[qp] = r;
+    } else {
+      g.counts[idx] = (uint16_t)max_iter;
+      if (COLOR) g.rgba[idx] = pal.interior;
+      QItem<float> r;
+      r.x = 0.f;
+      r.y = 0.f;
+      r.cnt = -1;  // nothing to replay
+      r.idx = idx;
+      items[qp] = r;
+    }
+  };
+  // initial slots: two grabs straight into the ring, then one per slot
+  refill();
+  if (!exhausted) refill();
+  {
+    const unsigned na = __popc(__ballot_sync(kFull, (unsigned)lane < rcount));
+    if ((unsigned)lane < rcount) {
+      take((unsigned)lane, X.x, Y.x, CR.x, CI.x, ca, ia, qa);
+      ha = true;
+    }
+    if ((unsigned)lane + na < rcount) {
+      take((unsigned)lane + na, X.y, Y.y, CR.y, CI.y, cb, ib, qb);
+      hb = true;
+    }
+    const unsigned used = min(rcount, 64u);
+    rhead = (rhead + used) & (kRing - 1);
+    rcount -= used;
+    if (!exhausted) refill();
+  }
+  const float2 HALF = make_float2(0.5f, 0.5f);
+  for (;;) {
+    if (!__any_sync(kFull, ha || hb)) break;
+    const float2 X0 = X, Y0 = Y;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const float2 YY = fmul2(Y, Y);
+      const float2 T = ffma2(X, X, fneg2(YY));
+      const float2 Yn = ffma2(X, Y, CI);
+      X = ffma2(T, HALF, CR);
+      Y = Yn;
+    }
+    const float2 M = ffma2(X, X, fmul2(Y, Y));
+    const bool ea = !(M.x <= 16.0f), eb = !(M.y <= 16.0f);  // unordered: NaN/inf escaped
+    const bool fa = ha && (ea || ca + K >= max_iter);
+    const bool fb = hb && (eb || cb + K >= max_iter);
+    if (ha && !fa) ca += K;
+    if (hb && !fb) cb += K;
+    const unsigned ma = __ballot_sync(kFull, fa), mb = __ballot_sync(kFull, fb);
+    if ((ma | mb) == 0u) continue;
+    if (fa) finish(ea, X0.x, Y0.x, ca, ia, qa);
+    if (fb) finish(eb, X0.y, Y0.y, cb, ib, qb);
+    const unsigned nfin = (unsigned)(__popc(ma) + __popc(mb));
+    while (rcount < nfin && !exhausted) refill();
+    const unsigned ra = (unsigned)__popc(ma & lt);
+    const unsigned rb = (unsigned)__popc(ma) + (unsigned)__popc(mb & lt);
+    if (fa) {
+      ha = ra < rcount;
+      if (ha) take(ra, X.x, Y.x, CR.x, CI.x, ca, ia, qa);
+    }
+    if (fb) {
+      hb = rb < rcount;
+      if (hb) take(rb, X.y, Y.y, CR.y, CI.y, cb, ib, qb);
+    }
+    const unsigned used = min(nfin, rcount);
+    rhead = (rhead + used) & (kRing - 1);
+    rcount -= used;
+    __syncwarp();
+    if (rcount < 32u && !exhausted) refill();
+  }
+  if (trace && lane == 0) trace[gw * 3 + 2] = global_ns();
+}
+
+// P3: exact escape index of P2X's replay records, one record per thread: the FAST step
+// with the per-iteration test from the recorded block-start state Z_cnt (the record's
+// block escaped at its end state, so the loop ends within K steps).  Resets the queue
+// header when the last CTA finishes (the next call's P1 appends from 0).
+template <bool MANDEL, bool COLOR, int K>
+__global__ void __launch_bounds__(kThreads)
+escape_replay_kernel(const Geom g, const Palette pal, const float jcr2, const float jci2,
+                     ContQueue* q, const QItem<float>* items) {
+  const unsigned n_items = *reinterpret_cast<volatile unsigned*>(&q->tail);
+  const unsigned stride = gridDim.x * kThreads;
+  for (unsigned i = blockIdx.x * kThreads + threadIdx.x; i < n_items; i += stride) {
+    const QItem<float> r = items[i];
+    if (r.cnt < 0) continue;
+    float x = r.x, y = r.y, cr = jcr2, ci = jci2;
+    if (MANDEL) {
+      const int row = (int)(r.idx / (unsigned)g.W);
+      const int px = (int)(r.idx - (unsigned)row * (unsigned)g.W);
+      cr = to_state<float, false>(pixel_re(g, px));
+      ci = to_state<float, false>(pixel_im(g, global_row(g, row)));
+    }
+    int j = 0;
+    for (; j < K; ++j) {
+      if (!(Iter<float, false>::mag(x, y) <= 16.0f)) break;
+      Iter<float, false>::core(x, y, cr, ci);
+    }
+    const int c0 = r.cnt + j;  // j == K: the block's end state (it escaped)
+    const int count = c0 < g.max_iter ? c0 : g.max_iter;
+    g.counts[r.idx] = (uint16_t)count;
+    if (COLOR) g.rgba[r.idx] = colour_dev(pal, count, g.max_iter);
+  }
+  // ---- self-reset of the queue by the last CTA
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&q->done_warps, 1u);
+    if (prev == gridDim.x - 1) {
+      q->tail = 0u;
+      q->head = 0u;
+      q->done_warps = 0u;
+      __threadfence();
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------------
 // Persistent lane-refill kernel (R) for one frame whose counts are heavy-tailed or long
 // (SURVEY §7 hard part 1).  Each warp owns a 32x8-pixel chunk at a time, taken from a
 // global atomic chunk counter (self-resetting workspace).  Every lane iterates its own

@@ -132,9 +132,17 @@ cudaError_t device_palette(fr::Palette& p, cudaStream_t s) {
   uchar4* ptr = nullptr;
   e = cudaMalloc(&ptr, p.n * sizeof(uchar4));
   if (e != cudaSuccess) return e;
-  e = cudaMemcpy(ptr, p.e, p.n * sizeof(uchar4), cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) return e;
+  // stream-ordered upload on the caller's stream, then wait for it: the copy is shared
+  // by later calls on any stream, which are not ordered after `s` (one-time cost)
   bucket.push_back(DevPalette{std::vector<uchar4>(p.e, p.e + p.n), ptr});
+  e = cudaMemcpyAsync(ptr, bucket.back().entries.data(), p.n * sizeof(uchar4),
+                      cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    bucket.pop_back();
+    cudaFree(ptr);
+    return e;
+  }
   p.dev = ptr;
   return cudaSuccess;
 }
@@ -290,8 +298,14 @@ cudaError_t workspace_for(cudaStream_t s, fr::Workspace** out) {
   fr::Workspace* w = nullptr;
   e = cudaMalloc(&w, sizeof(fr::Workspace));
   if (e != cudaSuccess) return e;
-  e = cudaMemset(w, 0, sizeof(fr::Workspace));
-  if (e != cudaSuccess) return e;
+  // zeroed in stream order on `s` (the first kernel to use it runs on `s`); the host
+  // waits once so that no later ordering question remains
+  e = cudaMemsetAsync(w, 0, sizeof(fr::Workspace), s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    cudaFree(w);
+    return e;
+  }
   g_ws[key] = w;
   *out = w;
   return cudaSuccess;
@@ -299,6 +313,7 @@ cudaError_t workspace_for(cudaStream_t s, fr::Workspace** out) {
 
 // Library-owned device buffers cached per (device, stream), grown on demand and created
 // outside any graph capture (like the workspace).
+std::vector<void*> g_retired;  // outgrown buffers, kept alive for captured graphs
 cudaError_t buffer_for(std::map<std::pair<int, uintptr_t>, std::pair<void*, size_t>>& g_cont,
                        cudaStream_t s, size_t bytes, void** out) {
   int dev = 0;
@@ -313,8 +328,10 @@ cudaError_t buffer_for(std::map<std::pair<int, uintptr_t>, std::pair<void*, size
   }
   if (capturing(s)) return cudaErrorStreamCaptureUnsupported;
   if (it != g_cont.end()) {
-    cudaStreamSynchronize(s);  // the old buffer may still be in use on this stream
-    cudaFree(it->second.first);
+    // Grown: the old buffer is NOT freed -- a CUDA graph captured earlier on this stream
+    // may still hold its address and be replayed later -- but parked until process exit
+    // (growth is rare: at most one step per frame size class).
+    g_retired.push_back(it->second.first);
     g_cont.erase(it);
   }
   void* p = nullptr;
@@ -416,7 +433,11 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   }
   cudaError_t e = buffer_for(g_queue, s, sizeof(fr::ContQueue), &qp);
   if (e != cudaSuccess) return e;
-  if (fresh && (e = cudaMemset(qp, 0, sizeof(fr::ContQueue))) != cudaSuccess) return e;
+  if (fresh) {  // zeroed in stream order on `s`, before P1 appends to it
+    e = cudaMemsetAsync(qp, 0, sizeof(fr::ContQueue), s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return e;
+  }
   auto* q = static_cast<fr::ContQueue*>(qp);
   void* ip = nullptr;
   e = buffer_for(g_items, s, (size_t)n * sizeof(fr::QItem<T>), &ip);
@@ -461,6 +482,47 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  // FP32_FAST under the precondition: the packed two-slot P2 (P2X) with a per-warp ring
+  // of queue items, then the replay kernel P3 for the exact escape indices
+  // (FRACTAL_P2X=0: the one-orbit amortised P2 below; FRACTAL_P2X_K: block 8/16/32)
+  if constexpr (!STRICT && std::is_same<T, float>::value) {
+    static const bool p2x = env_int("FRACTAL_P2X", 1) != 0;
+    if (amort && p2x) {
+      static const int kx = env_int("FRACTAL_P2X_K", 16);
+      auto k2 = fr::escape_cont2_kernel<MANDEL, COLOR, 16>;
+      auto k3 = fr::escape_replay_kernel<MANDEL, COLOR, 16>;
+      if (kx == 8) {
+        k2 = fr::escape_cont2_kernel<MANDEL, COLOR, 8>;
+        k3 = fr::escape_replay_kernel<MANDEL, COLOR, 8>;
+      } else if (kx == 32) {
+        k2 = fr::escape_cont2_kernel<MANDEL, COLOR, 32>;
+        k3 = fr::escape_replay_kernel<MANDEL, COLOR, 32>;
+      }
+      static const int occx = [&] {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k2, fr::kThreads, 0) !=
+                cudaSuccess || o <= 0)
+          o = 1;
+        return o;
+      }();
+      static const int occ_env = env_int("FRACTAL_P2_OCC", 0);
+      const int want = occ_env > 0 ? occ_env : 4;
+      const int o2 = want < occx ? want : occx;
+      k2<<<(unsigned)(sm_count() * o2), fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items);
+      e = cudaGetLastError();
+      if (e == cudaSuccess) {
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        k3<<<(unsigned)(sm_count() * 4), fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items);
+        e = cudaGetLastError();
+      }
+      if (e != cudaSuccess) {
+        cudaMemsetAsync(qp, 0, sizeof(fr::ContQueue), s);
+        return e;
+      }
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      return cudaSuccess;
+    }
+  }
   // P2 with the amortised block-end test when the escape-monotonicity precondition
   // holds (host-checked), else the exact per-iteration test
   // (strict modes never take the amortised kernel: it is not instantiated for them)

@@ -222,19 +222,29 @@ def render_path_sharded(cs, win, width: int, height: int, max_iter: int = 100, m
 
 
 def render_bands(kind: str, win, width: int, height: int, max_iter: int, band_rows: int,
-                 c: complex = 0j, mode=None, group=None, gather: bool = True, dst: int = 0):
+                 c: complex = 0j, mode=None, group=None, gather: bool = True, dst: int = 0,
+                 palette=None):
     """Each rank renders its cyclic bands of a Julia ('julia') or Mandelbrot
-    ('mandelbrot') frame; with gather=True the frame is assembled on dst."""
+    ('mandelbrot') frame, with the colour levels fused when `palette` is given (cfg3:
+    "fp32 + fused colorize, row bands"); with gather=True the frame (and its RGBA image)
+    is assembled on dst.  Returns counts, or (counts, rgba) with a palette; None for
+    both on ranks other than dst when gathering."""
     from . import binding as fr
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     bands = fr.Bands(band_rows, world, rank)
     if kind == "julia":
         mode = fr.Mode.FP32_FAST if mode is None else mode
-        local = fr.julia_render_ex(c, win, width, height, max_iter, mode, bands)
+        local = fr.julia_render_ex(c, win, width, height, max_iter, mode, bands,
+                                   palette=palette)
     else:
         mode = fr.Mode.FP64_FAST if mode is None else mode
-        local = fr.mandelbrot_param_map(win, width, height, max_iter, mode, bands)
+        local = fr.mandelbrot_param_map(win, width, height, max_iter, mode, bands,
+                                        palette=palette)
     if not gather:
         return local
-    return gather_bands(local, height, band_rows, dst, group)
+    if palette is None:
+        return gather_bands(local, height, band_rows, dst, group)
+    counts = gather_bands(local[0], height, band_rows, dst, group)
+    rgba = gather_bands(local[1], height, band_rows, dst, group)
+    return (counts, rgba) if counts is not None else (None, None)
