@@ -378,3 +378,55 @@ def julia_render_path_host(cs, win, width: int, height: int, max_iter: int = 100
                                        _stream(stream))
     _check(rc, "julia_render_path_host")
     return out
+
+
+class FramePlan:
+    """Latency path for repeated renders of one frame shape (the interactive case of
+    P:39 and the small frames of Fig. 1): every argument but C is validated and
+    marshalled ONCE -- output pointers, window, bands, palette and stream are kept as
+    ready ctypes objects -- so `render(c)` is one C-ABI call (julia_render_ex, or
+    mandelbrot_param_map for kind='mandelbrot', where C is ignored) plus the C value.
+    The output tensors are owned by the plan (`out`, `out_rgba`).  The calls it makes
+    are ordinary C-ABI calls, so a plan can also be captured into a CUDA graph (after
+    one eager render on the stream: the library's workspaces are created outside
+    capture, include/fractal.h "Memory")."""
+
+    def __init__(self, kind: str, win, width: int, height: int, max_iter: int = 100,
+                 mode: Mode = Mode.FP32_FAST, bands: Bands = FULL_FRAME, palette=None,
+                 out=None, out_rgba=None, stream=None):
+        import torch
+        if kind not in ("julia", "mandelbrot"):
+            raise FractalError(f"kind must be 'julia' or 'mandelbrot', got {kind!r}")
+        rows = height if bands is FULL_FRAME else band_local_rows(height, bands)
+        self.out = out if out is not None else torch.empty((rows, width), dtype=torch.uint16,
+                                                           device="cuda")
+        self._pal = _pal(palette) if palette is not None else None
+        if self._pal is not None and out_rgba is None:
+            out_rgba = torch.empty((rows, width, 4), dtype=torch.uint8, device="cuda")
+        self.out_rgba = out_rgba
+        self._p = _dev_ptr(self.out, "uint16", rows * width, "out")
+        self._q = (_dev_ptr(out_rgba, "uint8", rows * width * 4, "out_rgba")
+                   if out_rgba is not None else None)
+        self._palp = ctypes.byref(self._pal.c) if self._pal is not None else None
+        self._win = _window(win)
+        self._bands = bands._c()
+        self._stream = _stream(stream)
+        self._args = (width, height, max_iter, int(mode))
+        self._c = _Complex(0.0, 0.0)
+        lib = load()
+        self._fn = lib.julia_render_ex if kind == "julia" else lib.mandelbrot_param_map
+        self._julia = kind == "julia"
+
+    def render(self, c: complex = 0j):
+        """Enqueue the frame for C = c on the plan's stream; returns the output tensor(s)."""
+        if self._julia:
+            self._c.re = c.real
+            self._c.im = c.imag
+            rc = self._fn(self._c, self._win, *self._args, self._bands, self._p, self._palp,
+                          self._q, self._stream)
+        else:
+            rc = self._fn(self._win, *self._args, self._bands, self._p, self._palp, self._q,
+                          self._stream)
+        if rc:
+            _check(rc, "FramePlan.render")
+        return (self.out, self.out_rgba) if self._pal is not None else self.out

@@ -941,6 +941,10 @@ struct ContQueue {
   unsigned pad1[31];
   unsigned done_warps;
   unsigned pad2[31];
+  unsigned left;  // P2X: orbits handed over to the leftover launch (after the tail)
+  unsigned pad3[31];
+  unsigned head2;  // P2X leftover launch: items taken
+  unsigned pad4[31];
 };
 
 // KS > 0 (fast modes, under the escape-monotonicity precondition of kernel A / the
@@ -1376,54 +1380,82 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return _
 __device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ float2 fneg2(float2 a) { return make_float2(-a.x, -a.y); }
 
+// Slot life cycle.  A slot runs its orbit in blocks of K = NS sub-blocks of KS bare
+// iterations; the start state of every sub-block is kept (registers), so a slot whose
+// block end escaped records the start of the FIRST sub-block whose end escaped (by
+// monotonicity the later ones escaped too): P3 then replays at most KS steps.  A
+// finished slot takes its next orbit from its private stash (registers; no warp-
+// collective step); the warp refills empty stashes from its ring only when at least
+// kStashLow of them are empty or a slot went idle, and the ring from the queue in
+// prefetched grabs of 32.
+// phase 0: the survivors [0, tail) of P1.  Once the queue is dry a warp keeps running
+//   until it holds at most `donate` orbits, then appends those (current state, queue slot
+//   of their record) after the tail -- items[tail + left ...] -- marks their old record
+//   slots "nothing to replay" and exits, so the long drain of nearly empty warps is cut
+//   short (donate = 0: run to the end).
+// phase 1: the leftover launch over [tail, tail + left): the handed-over orbits packed
+//   densely into few warps, run to the end.
+constexpr int kStashLow = 16;
+
 template <bool MANDEL, bool COLOR, int K>
 __global__ void __launch_bounds__(kThreads)
 escape_cont2_kernel(const Geom g, const Palette pal, const float jcr2, const float jci2,
-                    ContQueue* q, QItem<float>* items) {
+                    ContQueue* q, QItem<float>* items, int phase, int donate) {
+  constexpr int KS = 8, NS = K / KS;
+  static_assert(K % KS == 0 && NS >= 1 && NS <= 4, "blocks of 1..4 sub-blocks of 8");
   __shared__ QItem<float> ring[kThreads / 32][kRing];
   __shared__ unsigned ringq[kThreads / 32][kRing];  // queue position of each ring entry
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const int max_iter = g.max_iter;
-  const unsigned n_items = *reinterpret_cast<volatile unsigned*>(&q->tail);
+  const unsigned tail = *reinterpret_cast<volatile unsigned*>(&q->tail);
+  const unsigned lo = phase == 0 ? 0u : tail;
+  const unsigned hi = phase == 0 ? tail : tail + *reinterpret_cast<volatile unsigned*>(&q->left);
+  unsigned* headp = phase == 0 ? &q->head : &q->head2;
   unsigned long long* trace = g_refill_trace;
   const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + warp;
-  if (trace && lane == 0) trace[gw * 3] = global_ns();
+  if (trace && lane == 0 && phase == 0) trace[gw * 3] = global_ns();
   QItem<float>* rg = ring[warp];
   unsigned* rq = ringq[warp];
   unsigned rhead = 0u, rcount = 0u;  // warp-uniform ring state
-  bool exhausted = false;
-  // refill: append one grab of up to 32 items to the ring (warp-collective)
-  auto refill = [&]() {
-    unsigned base = 0u;
-    if (lane == 0) base = atomicAdd(&q->head, 32u);
-    base = __shfl_sync(kFull, base, 0);
-    if (base >= n_items) {
-      exhausted = true;
-      if (trace && lane == 0) trace[gw * 3 + 1] = global_ns();
-      return;
-    }
-    const unsigned i = base + (unsigned)lane;
-    const unsigned slot = (rhead + rcount + (unsigned)lane) & (kRing - 1);
-    if (i < n_items) {
-      rg[slot] = items[i];
-      rq[slot] = i;
-    }
-    const unsigned got = min(32u, n_items - base);
-    rcount += got;
-    __syncwarp();
+  bool exhausted = false;            // no queue items left beyond the ring
+  unsigned pf_base = 0u;             // prefetched grab: base (lane 0 until loaded)
+  bool pf_valid = false, pf_loaded = false;
+  QItem<float> pf_item{};
+  auto reserve = [&]() {
+    if (lane == 0) pf_base = lo + atomicAdd(headp, 32u);
+    pf_valid = true;
+    pf_loaded = false;
   };
-
-  // slot state: .x = slot a, .y = slot b
-  float2 X = make_float2(0.f, 0.f), Y = X;
-  float2 CR = make_float2(jcr2, jcr2), CI = make_float2(jci2, jci2);
-  int ca = 0, cb = 0;           // iterations done before the current block
-  unsigned ia = 0u, ib = 0u;    // pixel index
-  unsigned qa = 0u, qb = 0u;    // queue position (replay record slot)
-  bool ha = false, hb = false;  // slot holds an orbit
-  auto take = [&](unsigned r, float& x, float& y, float& cr, float& ci, int& c, unsigned& idx,
-                  unsigned& qp) {
+  auto load = [&]() {
+    const unsigned base = __shfl_sync(kFull, pf_base, 0);
+    pf_base = base;
+    const unsigned i = base + (unsigned)lane;
+    if (i < hi) pf_item = items[i];
+    pf_loaded = true;
+  };
+  auto commit = [&]() {  // the prefetched grab into the ring; reserve the next one
+    if (!pf_loaded) load();
+    const unsigned base = pf_base;
+    pf_valid = false;
+    if (base < hi) {
+      const unsigned slot = (rhead + rcount + (unsigned)lane) & (kRing - 1);
+      if (base + (unsigned)lane < hi) {
+        rg[slot] = pf_item;
+        rq[slot] = base + (unsigned)lane;
+      }
+      rcount += min(32u, hi - base);
+      __syncwarp();
+    }
+    if (base + 32u < hi) {
+      reserve();
+    } else {
+      exhausted = true;
+      if (trace && lane == 0 && phase == 0) trace[gw * 3 + 1] = global_ns();
+    }
+  };
+  auto take = [&](unsigned r, float& x, float& y, int& c, unsigned& idx, unsigned& qp) {
     const unsigned s = (rhead + r) & (kRing - 1);
     const QItem<float> it = rg[s];
     x = it.x;
@@ -1431,92 +1463,175 @@ escape_cont2_kernel(const Geom g, const Palette pal, const float jcr2, const flo
     c = it.cnt;
     idx = it.idx;
     qp = rq[s];
-    if (MANDEL) {
-      const int row = (int)(idx / (unsigned)g.W);
-      const int px = (int)(idx - (unsigned)row * (unsigned)g.W);
-      cr = to_state<float, false>(pixel_re(g, px));
-      ci = to_state<float, false>(pixel_im(g, global_row(g, row)));
-    }
   };
-  // finished slot: interior (store) or replay record (over its consumed queue item)
-  auto finish = [&](bool esc, float x0, float y0, int c, unsigned idx, unsigned qp) {
-    if (esc) {
-      QItem<float> r;
-      r.x = x0;
-      r.y = y0;
-      r.cnt = c;
-      r.idx = idx;
-      items[qp] = r;
-    } else {
-      g.counts[idx] = (uint16_t)max_iter;
-      if (COLOR) g.rgba[idx] = pal.interior;
-      QItem<float> r;
-      r.x = 0.f;
-      r.y = 0.f;
-      r.cnt = -1;  // nothing to replay
-      r.idx = idx;
-      items[qp] = r;
-    }
+  auto c_of = [&](unsigned idx, float& cr, float& ci) {  // MANDEL: C from the pixel
+    const int row = (int)(idx / (unsigned)g.W);
+    const int px = (int)(idx - (unsigned)row * (unsigned)g.W);
+    cr = to_state<float, false>(pixel_re(g, px));
+    ci = to_state<float, false>(pixel_im(g, global_row(g, row)));
   };
-  // initial slots: two grabs straight into the ring, then one per slot
-  refill();
-  if (!exhausted) refill();
-  {
-    const unsigned na = __popc(__ballot_sync(kFull, (unsigned)lane < rcount));
-    if ((unsigned)lane < rcount) {
-      take((unsigned)lane, X.x, Y.x, CR.x, CI.x, ca, ia, qa);
-      ha = true;
+
+  // running slots (.x = slot a, .y = slot b) and their stashes
+  float2 X = make_float2(0.f, 0.f), Y = X;
+  float2 CR = make_float2(jcr2, jcr2), CI = make_float2(jci2, jci2);
+  int ca = 0, cb = 0;
+  unsigned ia = 0u, ib = 0u, qa = 0u, qb = 0u;
+  bool ha = false, hb = false;
+  float sxa = 0.f, sya = 0.f, sxb = 0.f, syb = 0.f;
+  int sca = 0, scb = 0;
+  unsigned sia = 0u, sib = 0u, sqa = 0u, sqb = 0u;
+  bool va = false, vb = false;  // stash valid
+  // fill the empty stashes from the ring (topping the ring up from the queue)
+  auto refill_stashes = [&]() {
+    const unsigned ea_m = __ballot_sync(kFull, !va), eb_m = __ballot_sync(kFull, !vb);
+    const unsigned need = (unsigned)(__popc(ea_m) + __popc(eb_m));
+    while (rcount < need && !exhausted) commit();
+    const unsigned ra = (unsigned)__popc(ea_m & lt);
+    const unsigned rb = (unsigned)__popc(ea_m) + (unsigned)__popc(eb_m & lt);
+    if (!va && ra < rcount) {
+      take(ra, sxa, sya, sca, sia, sqa);
+      va = true;
     }
-    if ((unsigned)lane + na < rcount) {
-      take((unsigned)lane + na, X.y, Y.y, CR.y, CI.y, cb, ib, qb);
-      hb = true;
+    if (!vb && rb < rcount) {
+      take(rb, sxb, syb, scb, sib, sqb);
+      vb = true;
     }
-    const unsigned used = min(rcount, 64u);
+    const unsigned used = min(need, rcount);
     rhead = (rhead + used) & (kRing - 1);
     rcount -= used;
-    if (!exhausted) refill();
-  }
+    __syncwarp();
+    if (rcount < 32u && !exhausted) commit();
+  };
+  // a free slot takes its stash
+  auto pull = [&]() {
+    if (!ha && va) {
+      X.x = sxa;
+      Y.x = sya;
+      ca = sca;
+      ia = sia;
+      qa = sqa;
+      if (MANDEL) c_of(ia, CR.x, CI.x);
+      ha = true;
+      va = false;
+    }
+    if (!hb && vb) {
+      X.y = sxb;
+      Y.y = syb;
+      cb = scb;
+      ib = sib;
+      qb = sqb;
+      if (MANDEL) c_of(ib, CR.y, CI.y);
+      hb = true;
+      vb = false;
+    }
+  };
+  reserve();
+  commit();
+  refill_stashes();
+  pull();
+  refill_stashes();
   const float2 HALF = make_float2(0.5f, 0.5f);
   for (;;) {
-    if (!__any_sync(kFull, ha || hb)) break;
-    const float2 X0 = X, Y0 = Y;
+    const unsigned hm = __ballot_sync(kFull, ha), hbm = __ballot_sync(kFull, hb);
+    if ((hm | hbm) == 0u) break;
+    if (exhausted && rcount == 0u && donate > 0 && !__any_sync(kFull, va || vb) &&
+        __popc(hm) + __popc(hbm) <= donate) {
+      // hand the held orbits to the leftover launch and leave
+      const unsigned n = (unsigned)(__popc(hm) + __popc(hbm));
+      unsigned base = 0u;
+      if (lane == 0) base = atomicAdd(&q->left, n);
+      base = tail + __shfl_sync(kFull, base, 0);
+      const unsigned ra = (unsigned)__popc(hm & lt);
+      const unsigned rb = (unsigned)__popc(hm) + (unsigned)__popc(hbm & lt);
+      QItem<float> skip;
+      skip.x = 0.f;
+      skip.y = 0.f;
+      skip.cnt = -1;
+      if (ha) {
+        QItem<float> it;
+        it.x = X.x; it.y = Y.x; it.cnt = ca; it.idx = ia;
+        items[base + ra] = it;
+        skip.idx = ia;
+        items[qa] = skip;
+      }
+      if (hb) {
+        QItem<float> it;
+        it.x = X.y; it.y = Y.y; it.cnt = cb; it.idx = ib;
+        items[base + rb] = it;
+        skip.idx = ib;
+        items[qb] = skip;
+      }
+      break;
+    }
+    float2 CX[NS], CY[NS];  // start state of each sub-block
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      const float2 YY = fmul2(Y, Y);
-      const float2 T = ffma2(X, X, fneg2(YY));
-      const float2 Yn = ffma2(X, Y, CI);
-      X = ffma2(T, HALF, CR);
-      Y = Yn;
+    for (int sb = 0; sb < NS; ++sb) {
+      CX[sb] = X;
+      CY[sb] = Y;
+#pragma unroll
+      for (int j = 0; j < KS; ++j) {
+        const float2 YY = fmul2(Y, Y);
+        const float2 T = ffma2(X, X, fneg2(YY));
+        const float2 Yn = ffma2(X, Y, CI);
+        X = ffma2(T, HALF, CR);
+        Y = Yn;
+      }
     }
     const float2 M = ffma2(X, X, fmul2(Y, Y));
     const bool ea = !(M.x <= 16.0f), eb = !(M.y <= 16.0f);  // unordered: NaN/inf escaped
     const bool fa = ha && (ea || ca + K >= max_iter);
     const bool fb = hb && (eb || cb + K >= max_iter);
+    if (pf_valid && !pf_loaded) load();  // stage the prefetched grab meanwhile
+    if (__any_sync(kFull, fa || fb)) {
+      // the escaping sub-block: the first whose end state (the next start) escaped
+      float xa = CX[NS - 1].x, ya = CY[NS - 1].x, xb = CX[NS - 1].y, yb = CY[NS - 1].y;
+      int oa = (NS - 1) * KS, ob = (NS - 1) * KS;
+#pragma unroll
+      for (int sb = NS - 2; sb >= 0; --sb) {
+        const float2 m = ffma2(CX[sb + 1], CX[sb + 1], fmul2(CY[sb + 1], CY[sb + 1]));
+        if (!(m.x <= 16.0f)) {
+          xa = CX[sb].x; ya = CY[sb].x; oa = sb * KS;
+        }
+        if (!(m.y <= 16.0f)) {
+          xb = CX[sb].y; yb = CY[sb].y; ob = sb * KS;
+        }
+      }
+      if (fa) {
+        QItem<float> r;
+        r.x = xa; r.y = ya; r.cnt = ea ? ca + oa : -1; r.idx = ia;
+        items[qa] = r;
+        if (!ea) {
+          g.counts[ia] = (uint16_t)max_iter;
+          if (COLOR) g.rgba[ia] = pal.interior;
+        }
+      }
+      if (fb) {
+        QItem<float> r;
+        r.x = xb; r.y = yb; r.cnt = eb ? cb + ob : -1; r.idx = ib;
+        items[qb] = r;
+        if (!eb) {
+          g.counts[ib] = (uint16_t)max_iter;
+          if (COLOR) g.rgba[ib] = pal.interior;
+        }
+      }
+      if (fa) ha = false;
+      if (fb) hb = false;
+      pull();
+    }
     if (ha && !fa) ca += K;
     if (hb && !fb) cb += K;
-    const unsigned ma = __ballot_sync(kFull, fa), mb = __ballot_sync(kFull, fb);
-    if ((ma | mb) == 0u) continue;
-    if (fa) finish(ea, X0.x, Y0.x, ca, ia, qa);
-    if (fb) finish(eb, X0.y, Y0.y, cb, ib, qb);
-    const unsigned nfin = (unsigned)(__popc(ma) + __popc(mb));
-    while (rcount < nfin && !exhausted) refill();
-    const unsigned ra = (unsigned)__popc(ma & lt);
-    const unsigned rb = (unsigned)__popc(ma) + (unsigned)__popc(mb & lt);
-    if (fa) {
-      ha = ra < rcount;
-      if (ha) take(ra, X.x, Y.x, CR.x, CI.x, ca, ia, qa);
+    // refill the stashes when enough are empty, or a slot is idle with orbits left
+    const unsigned empty = (unsigned)(__popc(__ballot_sync(kFull, !va)) +
+                                      __popc(__ballot_sync(kFull, !vb)));
+    if (empty >= (unsigned)kStashLow && (rcount > 0u || !exhausted)) {
+      refill_stashes();
+      pull();
+    } else if (__any_sync(kFull, !ha || !hb) && (rcount > 0u || !exhausted)) {
+      refill_stashes();
+      pull();
     }
-    if (fb) {
-      hb = rb < rcount;
-      if (hb) take(rb, X.y, Y.y, CR.y, CI.y, cb, ib, qb);
-    }
-    const unsigned used = min(nfin, rcount);
-    rhead = (rhead + used) & (kRing - 1);
-    rcount -= used;
-    __syncwarp();
-    if (rcount < 32u && !exhausted) refill();
   }
-  if (trace && lane == 0) trace[gw * 3 + 2] = global_ns();
+  if (trace && lane == 0 && phase == 0) trace[gw * 3 + 2] = global_ns();
 }
 
 // P3: exact escape index of P2X's replay records, one record per thread: the FAST step
@@ -1527,7 +1642,8 @@ template <bool MANDEL, bool COLOR, int K>
 __global__ void __launch_bounds__(kThreads)
 escape_replay_kernel(const Geom g, const Palette pal, const float jcr2, const float jci2,
                      ContQueue* q, const QItem<float>* items) {
-  const unsigned n_items = *reinterpret_cast<volatile unsigned*>(&q->tail);
+  const unsigned n_items = *reinterpret_cast<volatile unsigned*>(&q->tail) +
+                           *reinterpret_cast<volatile unsigned*>(&q->left);
   const unsigned stride = gridDim.x * kThreads;
   for (unsigned i = blockIdx.x * kThreads + threadIdx.x; i < n_items; i += stride) {
     const QItem<float> r = items[i];
@@ -1557,6 +1673,8 @@ escape_replay_kernel(const Geom g, const Palette pal, const float jcr2, const fl
     if (prev == gridDim.x - 1) {
       q->tail = 0u;
       q->head = 0u;
+      q->left = 0u;
+      q->head2 = 0u;
       q->done_warps = 0u;
       __threadfence();
     }

@@ -410,6 +410,11 @@ int twophase_budget(bool amort, bool f64) {
   return v < 4 ? 4 : v - v % 4;
 }
 
+bool p2x_on() {
+  static const bool v = env_int("FRACTAL_P2X", 0) != 0;  // off: slower so far
+  return v;
+}
+
 #ifndef FR_P1A_KS  // amortised P1 sub-block (0 = exact per-iteration test)
 #define FR_P1A_KS 0
 #endif
@@ -440,7 +445,9 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   }
   auto* q = static_cast<fr::ContQueue*>(qp);
   void* ip = nullptr;
-  e = buffer_for(g_items, s, (size_t)n * sizeof(fr::QItem<T>), &ip);
+  // (+ room for P2X's hand-over of at most 64 orbits per warp after the survivors)
+  const size_t extra = (size_t)sm_count() * 8 * (fr::kThreads / 32) * 64;
+  e = buffer_for(g_items, s, ((size_t)n + extra) * sizeof(fr::QItem<T>), &ip);
   if (e != cudaSuccess) return e;
   auto* items = static_cast<fr::QItem<T>*>(ip);
   // FRACTAL_P1_TILES=2: each P1 CTA renders two vertically adjacent tiles (exact P1 only)
@@ -483,20 +490,19 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   if (e != cudaSuccess) return e;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   // FP32_FAST under the precondition: the packed two-slot P2 (P2X) with a per-warp ring
-  // of queue items, then the replay kernel P3 for the exact escape indices
-  // (FRACTAL_P2X=0: the one-orbit amortised P2 below; FRACTAL_P2X_K: block 8/16/32)
+  // of queue items, its leftover launch for the orbits handed over by nearly empty warps
+  // once the queue is dry, then the replay kernel P3 for the exact escape indices
+  // (FRACTAL_P2X=0: the one-orbit amortised P2 below; FRACTAL_P2X_K: block 16/32;
+  // FRACTAL_P2X_D: hand-over threshold in held orbits per warp, 0 = none)
   if constexpr (!STRICT && std::is_same<T, float>::value) {
-    static const bool p2x = env_int("FRACTAL_P2X", 1) != 0;
-    if (amort && p2x) {
-      static const int kx = env_int("FRACTAL_P2X_K", 16);
-      auto k2 = fr::escape_cont2_kernel<MANDEL, COLOR, 16>;
-      auto k3 = fr::escape_replay_kernel<MANDEL, COLOR, 16>;
-      if (kx == 8) {
-        k2 = fr::escape_cont2_kernel<MANDEL, COLOR, 8>;
-        k3 = fr::escape_replay_kernel<MANDEL, COLOR, 8>;
-      } else if (kx == 32) {
-        k2 = fr::escape_cont2_kernel<MANDEL, COLOR, 32>;
-        k3 = fr::escape_replay_kernel<MANDEL, COLOR, 32>;
+    if (amort && p2x_on()) {
+      static const int kx = env_int("FRACTAL_P2X_K", 32);
+      static const int dx = env_int("FRACTAL_P2X_D", 16);
+      auto k2 = fr::escape_cont2_kernel<MANDEL, COLOR, 32>;
+      auto k3 = fr::escape_replay_kernel<MANDEL, COLOR, 32>;
+      if (kx == 16) {
+        k2 = fr::escape_cont2_kernel<MANDEL, COLOR, 16>;
+        k3 = fr::escape_replay_kernel<MANDEL, COLOR, 16>;
       }
       static const int occx = [&] {
         int o = 0;
@@ -506,13 +512,24 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
         return o;
       }();
       static const int occ_env = env_int("FRACTAL_P2_OCC", 0);
-      const int want = occ_env > 0 ? occ_env : 4;
+      const int want = occ_env > 0 ? occ_env : 2;
       const int o2 = want < occx ? want : occx;
-      k2<<<(unsigned)(sm_count() * o2), fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items);
+      const unsigned grid0 = (unsigned)(sm_count() * o2);
+      // leftover launch: at most `dx` orbits per phase-0 warp, 64 per warp after
+      const unsigned warps1 = (grid0 * (fr::kThreads / 32) * (unsigned)dx + 63u) / 64u;
+      const unsigned grid1 = (warps1 + fr::kThreads / 32 - 1) / (fr::kThreads / 32);
+      k2<<<grid0, fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items, 0, dx);
       e = cudaGetLastError();
       if (e == cudaSuccess) {
         g_launches.fetch_add(1, std::memory_order_relaxed);
-        k3<<<(unsigned)(sm_count() * 4), fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items);
+        if (dx > 0) {
+          k2<<<grid1 > 0 ? grid1 : 1u, fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items, 1, 0);
+          e = cudaGetLastError();
+          if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
+        }
+      }
+      if (e == cudaSuccess) {
+        k3<<<(unsigned)(sm_count() * 8), fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items);
         e = cudaGetLastError();
       }
       if (e != cudaSuccess) {
