@@ -352,6 +352,36 @@ def test_cfg5_strict_full_size_sampled(fr):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("mode", ["FP64_STRICT", "FP64_FAST"])
+def test_cfg5_full_frame_hash(fr, mode):
+    """cfg5 at full size, ALL of it: the GPU frame (16384^2, max_iter 10000, fp64) hashed
+    block by block against tests/golden/cfg5_oracle.json, which the committed
+    oracle-only script tools/oracle_cfg5_golden.py computed (parallel render ==
+    sequential render, bit for bit).  FP64_FAST compares against the FAST oracle's
+    hashes when they are present."""
+    import hashlib
+    import json
+    golden = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                         "cfg5_oracle.json")))
+    if mode not in golden:
+        pytest.skip(f"no oracle hashes for {mode} in cfg5_oracle.json")
+    ref = golden[mode]
+    cfg = W.configs()["cfg5"]
+    got = fr.mandelbrot_param_map(cfg.window, cfg.width, cfg.height, cfg.max_iter,
+                                  fr.Mode[mode])
+    torch.cuda.synchronize()
+    a = got.view(torch.int16).cpu().numpy().view(np.uint16)
+    del got
+    torch.cuda.empty_cache()
+    br = ref["block_rows"]
+    bad = [i for i, h in enumerate(ref["blocks"])
+           if hashlib.sha256(a[i * br:(i + 1) * br].astype("<u2").tobytes()).hexdigest() != h]
+    assert not bad, f"row blocks differing from the oracle: {bad}"
+    assert int(a.sum(dtype=np.int64)) == ref["sum_counts"]
+    assert int((a == cfg.max_iter).sum()) == ref["interior"]
+    assert hashlib.sha256(a.astype("<u2").tobytes()).hexdigest() == ref["sha256"]
+
+
 # ------------------------------------------------------------------ bands
 @pytest.mark.parametrize("n_ranks", [2, 4, 8])
 def test_bands_equal_rows_of_full_render(fr, n_ranks):
