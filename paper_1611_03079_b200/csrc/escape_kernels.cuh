@@ -341,8 +341,18 @@ __device__ __forceinline__ uchar4 colour_of(const uchar4* spal, const Palette& p
   return spal[c - q * p.n];
 }
 
+// What the kernels that read colours from the device copy need of a palette (S2, P1,
+// P2X, P3): 24 bytes of kernel parameters instead of the 1.1-KB Palette (the launch
+// copies every parameter byte; it matters for small frames).
+struct PalRef {
+  const uchar4* dev;
+  uchar4 interior;
+  uint32_t n;
+  uint32_t magic;
+};
+
 // The same colour level from the device copy of the palette (read-only path).
-__device__ __forceinline__ uchar4 colour_dev(const Palette& p, int cnt, int max_iter) {
+__device__ __forceinline__ uchar4 colour_dev(const PalRef& p, int cnt, int max_iter) {
   if (cnt == max_iter) return p.interior;
   const unsigned c = (unsigned)cnt;
   const unsigned q = __umulhi(c, p.magic);
@@ -837,6 +847,88 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
 }
 
 // ----------------------------------------------------------------------------------
+// Kernel SX: C-path frames in FP32_FAST (Julia), two x-adjacent pixels per lane.  CTA tile
+// 64 x 8 pixels, warp tile 16 x 4: lane l holds pixels (2 (l & 7), l >> 3) and
+// (2 (l & 7) + 1, l >> 3) of its warp tile as the two halves of the packed FFMA2 vote
+// loop, both with the frame's C.  A warp row is then 16 pixels = one whole 32-byte
+// sector of uint16 counts, written by one 4-byte store per lane: no sector is shared
+// between warps, so no partially written sector is ever evicted from L2 (with 8 x 4
+// warp tiles every sector was split between two warps that drift apart over the frame
+// group: +0.4 GB of DRAM read-modify-write per bench launch).
+// The CTA renders a group of `fpc` frames of the path chunk for its tile (pixel map
+// amortised over the group), one frame at a time.
+// ----------------------------------------------------------------------------------
+constexpr int kTileWX = 64;
+template <int NC, int ES, bool COLOR>
+__global__ void __launch_bounds__(kThreads)
+escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, int frame0,
+                    int n_frames, int fpc) {
+  using CountT = typename std::conditional<ES == 2, uint16_t, uint8_t>::type;
+  int tx, ty, grp;
+  tile_of(g, tx, ty, grp);  // g.tiles_x counts 64-pixel tiles here
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int px = tx * kTileWX + (warp & 3) * 16 + (lane & 7) * 2;
+  const int ly = ty * kTileH + (warp >> 2) * 4 + (lane >> 3);
+  const bool in0 = px < g.W && ly < g.rows;
+  const bool in1 = px + 1 < g.W && ly < g.rows;
+  const float re0 = to_state<float, false>(pixel_re(g, min(px, g.W - 1)));
+  const float re1 = to_state<float, false>(pixel_re(g, min(px + 1, g.W - 1)));
+  const float im = to_state<float, false>(pixel_im(g, global_row(g, min(ly, g.rows - 1))));
+  const int max_iter = g.max_iter;
+  const int kfull = max_iter - max_iter % 4;
+  const int f0 = grp * fpc;
+  const int f1 = min(f0 + fpc, n_frames);
+  const int64_t stride = g.frame_stride;
+  const int64_t pix0 = (int64_t)(frame0 + f0) * stride + (int64_t)ly * g.W + px;
+  CountT* outp = (ES == 2 ? reinterpret_cast<CountT*>(g.counts)
+                          : reinterpret_cast<CountT*>(g.counts8)) + pix0;
+  uchar4* outc = COLOR ? g.rgba + pix0 : nullptr;
+  // one store for both counts when the pair is whole and aligned in every frame
+  const uintptr_t base_c = ES == 2 ? reinterpret_cast<uintptr_t>(g.counts)
+                                   : reinterpret_cast<uintptr_t>(g.counts8);
+  const bool vec = in1 && ((g.W & 1) == 0) && ((stride & 1) == 0) &&
+                   (base_c % (2 * ES)) == 0 &&
+                   (!COLOR || (reinterpret_cast<uintptr_t>(g.rgba) & 7) == 0);
+  for (int f = f0; f < f1; ++f) {
+    float x = re0, y = im, x2 = re1, y2 = im;
+    unsigned alive = in0 ? 1u : 0u, alive2 = in1 ? 1u : 0u;
+    int cnt = 0, cnt2 = 0;
+    const float cr = cs.re[f], ci = cs.im[f];
+    int n = fast_vote_loop2x_f32<4>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr, ci,
+                                    kfull);
+    if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
+      for (; n < max_iter; ++n) {
+        Iter<float, false>::step(x, y, cr, ci, alive, cnt);
+        Iter<float, false>::step(x2, y2, cr, ci, alive2, cnt2);
+      }
+    }
+    if (vec) {
+      if constexpr (ES == 2)
+        *reinterpret_cast<uint32_t*>(outp) = (uint32_t)cnt | ((uint32_t)cnt2 << 16);
+      else
+        *reinterpret_cast<uint16_t*>(outp) = (uint16_t)(cnt | (cnt2 << 8));
+      if (COLOR) {
+        const uchar4 a = colour_dev(pal, cnt, max_iter), b = colour_dev(pal, cnt2, max_iter);
+        *reinterpret_cast<uint2*>(outc) =
+            make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+      }
+    } else {
+      if (in0) {
+        outp[0] = (CountT)cnt;
+        if (COLOR) outc[0] = colour_dev(pal, cnt, max_iter);
+      }
+      if (in1) {
+        outp[1] = (CountT)cnt2;
+        if (COLOR) outc[1] = colour_dev(pal, cnt2, max_iter);
+      }
+    }
+    outp += stride;
+    if (COLOR) outc += stride;
+  }
+}
+
+// ----------------------------------------------------------------------------------
 // Static-tile kernel for ONE frame, fp32 (fast or strict), two pixels per thread (S2): CTA tile
 // 32x16, each thread iterates the pixels of rows ly and ly + 8 of its 8x4-lane warp
 // tile together in the two-orbit PTX vote loop (ILP for the FP pipe, one vote for
@@ -845,7 +937,7 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
 // ----------------------------------------------------------------------------------
 template <bool STRICT, bool MANDEL, bool COLOR, int KV = 4>
 __global__ void __launch_bounds__(kThreads)
-escape_tile2_kernel(const Geom g, const Palette pal, const float jcr2, const float jci2) {
+escape_tile2_kernel(const Geom g, const PalRef pal, const float jcr2, const float jci2) {
   // jcr2/jci2: the Julia C in the state representation (doubled in FAST, plain in STRICT)
   // colours from the device palette (no CTA barrier in these short-lived CTAs)
   int tx, ty, grp;
@@ -956,7 +1048,7 @@ struct ContQueue {
 // PRE > 0: the first PRE iterations run the exact vote loop (counts of the orbits that
 // end there are final); the amortised sub-blocks continue the rest from PRE.
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int KS, int PRE, int KV>
-__device__ __forceinline__ void budget_tile(const Geom& g, const Palette& pal, const T jcr,
+__device__ __forceinline__ void budget_tile(const Geom& g, const PalRef& pal, const T jcr,
                                             const T jci, int budget, ContQueue* q,
                                             QItem<T>* items, const int tx, const int ty) {
   // CTA tile 32x16: each thread iterates the pixels of rows ly and ly + 8 of its 8x4-lane
@@ -1116,7 +1208,7 @@ __device__ __forceinline__ void budget_tile(const Geom& g, const Palette& pal, c
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int KS = 0, int PRE = 0, int KV = 4,
           int NT = 1>
 __global__ void __launch_bounds__(kThreads)
-escape_budget_kernel(const Geom g, const Palette pal, const T jcr, const T jci, int budget,
+escape_budget_kernel(const Geom g, const PalRef pal, const T jcr, const T jci, int budget,
                      ContQueue* q, QItem<T>* items) {
   int tx, ty, grp;
   tile_of(g, tx, ty, grp);
@@ -1399,7 +1491,7 @@ constexpr int kStashLow = 16;
 
 template <bool MANDEL, bool COLOR, int K>
 __global__ void __launch_bounds__(kThreads)
-escape_cont2_kernel(const Geom g, const Palette pal, const float jcr2, const float jci2,
+escape_cont2_kernel(const Geom g, const PalRef pal, const float jcr2, const float jci2,
                     ContQueue* q, QItem<float>* items, int phase, int donate) {
   constexpr int KS = 8, NS = K / KS;
   static_assert(K % KS == 0 && NS >= 1 && NS <= 4, "blocks of 1..4 sub-blocks of 8");
@@ -1634,13 +1726,218 @@ escape_cont2_kernel(const Geom g, const Palette pal, const float jcr2, const flo
   if (trace && lane == 0 && phase == 0) trace[gw * 3 + 2] = global_ns();
 }
 
+// ----------------------------------------------------------------------------------
+// "P2T": the one-orbit amortised P2 (escape_cont_kernel<..., AMORT>) in packed form, for
+// FP32_FAST under the escape-monotonicity precondition.  Each lane runs two orbits
+// (slots a, b) as the halves of float2 registers (FFMA2/FMUL2).  Blocks of K = NS x KS
+// bare iterations with the sub-block start states kept; at a block end a slot whose
+// end state escaped (or that reached the iteration limit) notes the start of its
+// escaping sub-block and FREEZES (done).  When at least TH of the warp's 64 slots are
+// done (all of them once the queue is dry), the warp services them together: one packed
+// replay of <= KS steps with the per-iteration test recovers every exact escape index,
+// the counts (and colours) are stored, and the freed slots are refilled from the staged
+// grab of 32 queue items (next grab prefetched, as in the one-orbit P2).
+// ----------------------------------------------------------------------------------
+template <bool MANDEL, bool COLOR, int K, int TH>
+__global__ void __launch_bounds__(kThreads)
+escape_cont2t_kernel(const Geom g, const PalRef pal, const float jcr2, const float jci2,
+                     ContQueue* q, const QItem<float>* items) {
+  constexpr int KS = 8, NS = K / KS;
+  static_assert(K % KS == 0 && NS >= 1 && NS <= 8, "blocks of sub-blocks of 8");
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int max_iter = g.max_iter;
+  const unsigned n_items = *reinterpret_cast<volatile unsigned*>(&q->tail);
+  unsigned long long* trace = g_refill_trace;
+  const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (trace && lane == 0) trace[gw * 3] = global_ns();
+  // staged grabs of 32 queue items (one per lane), as in escape_cont_kernel
+  bool exhausted = false;
+  unsigned cbase = 0u, gpos = 0u, gend = 0u;
+  QItem<float> cur{}, nxt{};
+  unsigned nbase = 0u, pf = 0u;
+  bool nxt_loaded = false, pf_issued = false;
+  auto load_grab = [&](unsigned base, QItem<float>& dst) {
+    if (base + (unsigned)lane < n_items) dst = items[base + (unsigned)lane];
+  };
+  // slots (.x = a, .y = b)
+  float2 X = make_float2(0.f, 0.f), Y = X;
+  float2 CR = make_float2(jcr2, jcr2), CI = make_float2(jci2, jci2);
+  int ca = 0, cb = 0;                    // iterations done before the current block
+  unsigned ia = 0u, ib = 0u;             // pixel index
+  bool ha = false, hb = false;           // holds an orbit
+  bool da = false, db = false;           // finished, awaiting service
+  bool ea = false, eb = false;           // finished by escape (else: iteration limit)
+  float2 RX = X, RY = X;                 // replay start (escaping sub-block)
+  int ra = 0, rb = 0;                    // its iteration index
+  auto c_of = [&](unsigned idx, float& cr, float& ci) {
+    const int row = (int)(idx / (unsigned)g.W);
+    const int px = (int)(idx - (unsigned)row * (unsigned)g.W);
+    cr = to_state<float, false>(pixel_re(g, px));
+    ci = to_state<float, false>(pixel_im(g, global_row(g, row)));
+  };
+  // give every free slot an item (slots a first, then b), fetching grabs as needed
+  auto dispense = [&]() {
+    unsigned na = __ballot_sync(kFull, !ha), nb = __ballot_sync(kFull, !hb);
+    while ((na | nb) != 0u && !exhausted) {
+      if (gpos >= gend) {
+        if (!nxt_loaded) {
+          unsigned base = 0u;
+          if (lane == 0) base = pf_issued ? pf : atomicAdd(&q->head, 32u);
+          nbase = __shfl_sync(kFull, base, 0);
+          pf_issued = false;
+          if (nbase < n_items) load_grab(nbase, nxt);
+        }
+        nxt_loaded = false;
+        if (nbase >= n_items) {
+          exhausted = true;
+          if (trace && lane == 0) trace[gw * 3 + 1] = global_ns();
+          break;
+        }
+        cur = nxt;
+        cbase = nbase;
+        gpos = nbase;
+        gend = min(nbase + 32u, n_items);
+        if (gend < n_items) {
+          if (lane == 0) pf = atomicAdd(&q->head, 32u);
+          pf_issued = true;
+        }
+      }
+      const unsigned avail = gend - gpos;
+      const unsigned rka = (unsigned)__popc(na & lt);
+      const unsigned rkb = (unsigned)__popc(na) + (unsigned)__popc(nb & lt);
+      const bool wa = ((na >> lane) & 1u) && rka < avail;
+      const bool wb = ((nb >> lane) & 1u) && rkb < avail;
+      const int sa = (int)(gpos - cbase + (rka < avail ? rka : 0u));
+      const int sb = (int)(gpos - cbase + (rkb < avail ? rkb : 0u));
+      const float xa_ = __shfl_sync(kFull, cur.x, sa), ya_ = __shfl_sync(kFull, cur.y, sa);
+      const int ka_ = __shfl_sync(kFull, cur.cnt, sa);
+      const unsigned ja_ = __shfl_sync(kFull, cur.idx, sa);
+      const float xb_ = __shfl_sync(kFull, cur.x, sb), yb_ = __shfl_sync(kFull, cur.y, sb);
+      const int kb_ = __shfl_sync(kFull, cur.cnt, sb);
+      const unsigned jb_ = __shfl_sync(kFull, cur.idx, sb);
+      if (wa) {
+        X.x = xa_; Y.x = ya_; ca = ka_; ia = ja_; ha = true;
+        if (MANDEL) c_of(ia, CR.x, CI.x);
+      }
+      if (wb) {
+        X.y = xb_; Y.y = yb_; cb = kb_; ib = jb_; hb = true;
+        if (MANDEL) c_of(ib, CR.y, CI.y);
+      }
+      const unsigned want = (unsigned)(__popc(na) + __popc(nb));
+      gpos += want < avail ? want : avail;
+      na = __ballot_sync(kFull, !ha);
+      nb = __ballot_sync(kFull, !hb);
+      if (!pf_issued || nxt_loaded || gpos >= gend) continue;
+      // the prefetch atomic has had a dispense round to return: stage its items
+      nbase = __shfl_sync(kFull, pf, 0);
+      pf_issued = false;
+      nxt_loaded = true;
+      if (nbase < n_items) load_grab(nbase, nxt);
+    }
+  };
+  dispense();
+  const float2 HALF = make_float2(0.5f, 0.5f);
+  for (;;) {
+    const int n_held = __popc(__ballot_sync(kFull, ha)) + __popc(__ballot_sync(kFull, hb));
+    if (n_held == 0) break;
+    float2 CX[NS], CY[NS];
+#pragma unroll
+    for (int s2 = 0; s2 < NS; ++s2) {
+      CX[s2] = X;
+      CY[s2] = Y;
+#pragma unroll
+      for (int j = 0; j < KS; ++j) {
+        const float2 YY = fmul2(Y, Y);
+        const float2 T = ffma2(X, X, fneg2(YY));
+        const float2 Yn = ffma2(X, Y, CI);
+        X = ffma2(T, HALF, CR);
+        Y = Yn;
+      }
+    }
+    const float2 M = ffma2(X, X, fmul2(Y, Y));
+    const bool xa = !(M.x <= 16.0f), xb = !(M.y <= 16.0f);  // unordered: NaN/inf escaped
+    const bool fa = ha && !da && (xa || ca + K >= max_iter);
+    const bool fb = hb && !db && (xb || cb + K >= max_iter);
+    if (__any_sync(kFull, fa || fb)) {
+      // escaping sub-block = the first whose end state (the next start) escaped
+      float2 sx = CX[NS - 1], sy = CY[NS - 1];
+      int oa = (NS - 1) * KS, ob = (NS - 1) * KS;
+#pragma unroll
+      for (int s2 = NS - 2; s2 >= 0; --s2) {
+        const float2 m = ffma2(CX[s2 + 1], CX[s2 + 1], fmul2(CY[s2 + 1], CY[s2 + 1]));
+        if (!(m.x <= 16.0f)) { sx.x = CX[s2].x; sy.x = CY[s2].x; oa = s2 * KS; }
+        if (!(m.y <= 16.0f)) { sx.y = CX[s2].y; sy.y = CY[s2].y; ob = s2 * KS; }
+      }
+      if (fa) { RX.x = sx.x; RY.x = sy.x; ra = ca + oa; ea = xa; da = true; }
+      if (fb) { RX.y = sx.y; RY.y = sy.y; rb = cb + ob; eb = xb; db = true; }
+    }
+    if (ha && !da) ca += K;
+    if (hb && !db) cb += K;
+    const int n_done = __popc(__ballot_sync(kFull, da)) + __popc(__ballot_sync(kFull, db));
+    const int thr = exhausted ? n_held : (TH < n_held ? TH : n_held);
+    if (n_done < thr || n_done == 0) continue;
+    // ---- service: packed replay of the escaped slots, stores, refill
+    {
+      bool pa = da && ea, pb = db && eb;  // still searching
+      int na_ = 0, nb_ = 0;
+      float2 x = RX, y = RY;
+#pragma unroll 1
+      for (int j = 0; j <= KS; ++j) {
+        if (!__any_sync(kFull, pa || pb)) break;
+        const float2 m = ffma2(x, x, fmul2(y, y));
+        pa = pa && (m.x <= 16.0f);
+        pb = pb && (m.y <= 16.0f);
+        if (pa) ++na_;
+        if (pb) ++nb_;
+        const float2 YY = fmul2(y, y);
+        const float2 T = ffma2(x, x, fneg2(YY));
+        const float2 Yn = ffma2(x, y, CI);
+        x = ffma2(T, HALF, CR);
+        y = Yn;
+      }
+      if (da) {
+        const int c0 = ea ? ra + na_ : max_iter;
+        const int count = c0 < max_iter ? c0 : max_iter;
+        g.counts[ia] = (uint16_t)count;
+        if (COLOR) g.rgba[ia] = colour_dev(pal, count, max_iter);
+        ha = false;
+        da = false;
+      }
+      if (db) {
+        const int c0 = eb ? rb + nb_ : max_iter;
+        const int count = c0 < max_iter ? c0 : max_iter;
+        g.counts[ib] = (uint16_t)count;
+        if (COLOR) g.rgba[ib] = colour_dev(pal, count, max_iter);
+        hb = false;
+        db = false;
+      }
+    }
+    dispense();
+  }
+  if (trace && lane == 0) trace[gw * 3 + 2] = global_ns();
+  // ---- self-reset of the queue by the last warp to finish
+  if (lane == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&q->done_warps, 1u);
+    if (prev == gridDim.x * (kThreads / 32) - 1) {
+      q->tail = 0u;
+      q->head = 0u;
+      q->left = 0u;
+      q->head2 = 0u;
+      q->done_warps = 0u;
+      __threadfence();
+    }
+  }
+}
+
 // P3: exact escape index of P2X's replay records, one record per thread: the FAST step
 // with the per-iteration test from the recorded block-start state Z_cnt (the record's
 // block escaped at its end state, so the loop ends within K steps).  Resets the queue
 // header when the last CTA finishes (the next call's P1 appends from 0).
 template <bool MANDEL, bool COLOR, int K>
 __global__ void __launch_bounds__(kThreads)
-escape_replay_kernel(const Geom g, const Palette pal, const float jcr2, const float jci2,
+escape_replay_kernel(const Geom g, const PalRef pal, const float jcr2, const float jci2,
                      ContQueue* q, const QItem<float>* items) {
   const unsigned n_items = *reinterpret_cast<volatile unsigned*>(&q->tail) +
                            *reinterpret_cast<volatile unsigned*>(&q->left);

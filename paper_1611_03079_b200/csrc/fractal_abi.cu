@@ -147,6 +147,15 @@ cudaError_t device_palette(fr::Palette& p, cudaStream_t s) {
   return cudaSuccess;
 }
 
+fr::PalRef pal_ref(const fr::Palette& p) {
+  fr::PalRef r;
+  r.dev = p.dev;
+  r.interior = p.interior;
+  r.n = p.n;
+  r.magic = p.magic;
+  return r;
+}
+
 // Parameter derivation in binary64: hx = half_w / W, hy = half_h / H.
 fr::Geom make_geom(fr_window win, int32_t width, int32_t height, int32_t max_iter,
                    fr_bands b, int64_t rows, uint16_t* counts, uint8_t* rgba) {
@@ -200,13 +209,35 @@ cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr:
       if constexpr (!STRICT) {
         if (vote_k() == 2) k2 = fr::escape_tile2_kernel<STRICT, MANDEL, COLOR, 2>;
       }
-      k2<<<grid2, fr::kThreads, 0, s>>>(g, pal, cs.re[0], cs.im[0]);
+      k2<<<grid2, fr::kThreads, 0, s>>>(g, pal_ref(pal), cs.re[0], cs.im[0]);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      return cudaGetLastError();
+    }
+  }
+  // C-path frames in FP32_FAST: kernel SX (x-adjacent pixel pairs, whole-sector count
+  // stores; FRACTAL_SX=0 keeps kernel S's frame pairs)
+  if constexpr (NC > 1 && !STRICT && !MANDEL && std::is_same<T, float>::value) {
+    static const bool sx = !env_is("FRACTAL_SX", "0");
+    if (sx) {
+      fr::Geom gx = g;
+      gx.tiles_x = (g.W + fr::kTileWX - 1) / fr::kTileWX;
+      const dim3 gridx =
+          tile_grid(gx, (g.rows + fr::kTileH - 1) / fr::kTileH, (n_frames + fpc - 1) / fpc);
+      if (g.counts8 != nullptr)
+        fr::escape_pathx_kernel<NC, 1, COLOR>
+            <<<gridx, fr::kThreads, 0, s>>>(gx, pal_ref(pal), cs, frame0, n_frames, fpc);
+      else
+        fr::escape_pathx_kernel<NC, 2, COLOR>
+            <<<gridx, fr::kThreads, 0, s>>>(gx, pal_ref(pal), cs, frame0, n_frames, fpc);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return cudaGetLastError();
     }
   }
   const dim3 grid = tile_grid(g, (g.rows + fr::kTileH - 1) / fr::kTileH, (n_frames + fpc - 1) / fpc);
-  constexpr int KD = sizeof(T) == 8 ? 2 * kStaticK : kStaticK;
+#ifndef FR_STATIC_K_FAST  // vote block of kernel S's fast fp32 frame pairs (A/B knob)
+#define FR_STATIC_K_FAST kStaticK
+#endif
+  constexpr int KD = sizeof(T) == 8 ? 2 * kStaticK : (STRICT ? kStaticK : FR_STATIC_K_FAST);
   if (g.counts8 != nullptr) {  // uint8 counts: path chunks only (julia_render_path8)
     if constexpr (NC > 1 && !MANDEL)
       fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, KD, NC, 0, 1>
@@ -232,6 +263,12 @@ T state_of(double v) {
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int NC>
 cudaError_t launch_tiles_conv(const fr::Geom& g, const fr::Palette& pal, const fr_complex* c,
                               int n_frames, int frame0, cudaStream_t s) {
+  if constexpr (NC == 1) {  // single frames: no heap round trip (small-frame latency)
+    fr::CList<T, 1> one;
+    one.re[0] = MANDEL ? T(0) : state_of<T, STRICT>(c[0].re);
+    one.im[0] = MANDEL ? T(0) : state_of<T, STRICT>(c[0].im);
+    return launch_tiles_t<T, STRICT, MANDEL, COLOR, 1>(g, pal, one, n_frames, frame0, s);
+  }
   fr::CList<T, NC>* cs = new (std::nothrow) fr::CList<T, NC>;
   if (!cs) return cudaErrorMemoryAllocation;
   for (int k = 0; k < n_frames && !MANDEL; ++k) {
@@ -410,6 +447,11 @@ int twophase_budget(bool amort, bool f64) {
   return v < 4 ? 4 : v - v % 4;
 }
 
+bool p2t_on() {
+  static const bool v = env_int("FRACTAL_P2T", 0) != 0;  // off: slower
+  return v;
+}
+
 bool p2x_on() {
   static const bool v = env_int("FRACTAL_P2X", 0) != 0;  // off: slower so far
   return v;
@@ -485,10 +527,42 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   // the two-tile CTA is the exact P1 alone (it overrides the other P1 knobs): its grid
   // covers half as many tile rows
   if (p1nt == 2) kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 0, 0, 4, 2>;
-  kern1<<<grid1, fr::kThreads, 0, s>>>(g, pal, jcr, jci, budget, q, items);
+  kern1<<<grid1, fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, budget, q, items);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  // FP32_FAST under the precondition: the packed two-slot P2 with threshold service
+  // (P2T; FRACTAL_P2T=0 falls back; FRACTAL_P2T_TH: service threshold of 64 slots)
+  if constexpr (!STRICT && std::is_same<T, float>::value) {
+    if (amort && p2t_on()) {
+      static const int th = env_int("FRACTAL_P2T_TH", 16);
+      auto kt = fr::escape_cont2t_kernel<MANDEL, COLOR, 32, 16>;
+      if (th == 8) kt = fr::escape_cont2t_kernel<MANDEL, COLOR, 32, 8>;
+      else if (th == 24) kt = fr::escape_cont2t_kernel<MANDEL, COLOR, 32, 24>;
+      else if (th == 32) kt = fr::escape_cont2t_kernel<MANDEL, COLOR, 32, 32>;
+      else if (th == 116) kt = fr::escape_cont2t_kernel<MANDEL, COLOR, 16, 16>;
+      else if (th == 164) kt = fr::escape_cont2t_kernel<MANDEL, COLOR, 64, 16>;
+      static const int occt = [&] {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kt, fr::kThreads, 0) !=
+                cudaSuccess || o <= 0)
+          o = 1;
+        return o;
+      }();
+      static const int occ_env = env_int("FRACTAL_P2_OCC", 0);
+      const int want = occ_env > 0 ? occ_env : 3;
+      const int o2 = want < occt ? want : occt;
+      kt<<<(unsigned)(sm_count() * o2), fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, q,
+                                                              items);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        cudaMemsetAsync(qp, 0, sizeof(fr::ContQueue), s);
+        return e;
+      }
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      return cudaSuccess;
+    }
+  }
   // FP32_FAST under the precondition: the packed two-slot P2 (P2X) with a per-warp ring
   // of queue items, its leftover launch for the orbits handed over by nearly empty warps
   // once the queue is dry, then the replay kernel P3 for the exact escape indices
@@ -518,18 +592,18 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
       // leftover launch: at most `dx` orbits per phase-0 warp, 64 per warp after
       const unsigned warps1 = (grid0 * (fr::kThreads / 32) * (unsigned)dx + 63u) / 64u;
       const unsigned grid1 = (warps1 + fr::kThreads / 32 - 1) / (fr::kThreads / 32);
-      k2<<<grid0, fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items, 0, dx);
+      k2<<<grid0, fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, q, items, 0, dx);
       e = cudaGetLastError();
       if (e == cudaSuccess) {
         g_launches.fetch_add(1, std::memory_order_relaxed);
         if (dx > 0) {
-          k2<<<grid1 > 0 ? grid1 : 1u, fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items, 1, 0);
+          k2<<<grid1 > 0 ? grid1 : 1u, fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, q, items, 1, 0);
           e = cudaGetLastError();
           if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
         }
       }
       if (e == cudaSuccess) {
-        k3<<<(unsigned)(sm_count() * 8), fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items);
+        k3<<<(unsigned)(sm_count() * 8), fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, q, items);
         e = cudaGetLastError();
       }
       if (e != cudaSuccess) {
@@ -852,6 +926,8 @@ static fr_status render_path_impl(const fr_complex* c_host, int32_t n_frames, fr
                          out_rgba);
   g.counts8 = out8;
   cudaError_t e = cudaSuccess;
+  // kernel SX reads colours from the device copy of the palette
+  if (pal != nullptr && (e = device_palette(p, stream)) != cudaSuccess) return cuda_status(e);
   for (int32_t f0 = 0; f0 < n_frames && e == cudaSuccess; f0 += fr::kMaxPathChunk) {
     const int nf = n_frames - f0 < fr::kMaxPathChunk ? n_frames - f0 : fr::kMaxPathChunk;
     e = launch_tiles<false, fr::kMaxPathChunk>(mode, pal != nullptr, g, p, c_host + f0, nf, f0,

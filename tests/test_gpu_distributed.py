@@ -81,3 +81,47 @@ def test_deliver_path_nccl(nccl, chunk):
     np.testing.assert_array_equal(got.to_path_order().cpu().numpy(), ref.cpu().numpy())
     for k in (0, 11, 22):
         np.testing.assert_array_equal(got.frame(k).cpu().numpy(), ref[k].cpu().numpy())
+
+
+def test_render_bands_with_palette_nccl(nccl):
+    """cfg3-style bands with the fused palette (BASELINE configs[2]: "fp32 + fused
+    colorize, row bands"): counts and RGBA gathered equal one full render."""
+    from paper_1611_03079_b200 import binding as fr
+    from paper_1611_03079_b200 import distributed as D
+    from paper_1611_03079_b200 import workloads as W
+    w, h, br = 640, 361, 15
+    win = W.julia_window(w, h)
+    pal = W.palette("classic")
+    c = -0.7269 + 0.1889j
+    counts, rgba = D.render_bands("julia", win, w, h, 1000, br, c=c, mode=fr.Mode.FP32_FAST,
+                                  palette=pal)
+    full, full_rgba = fr.julia_render_ex(c, win, w, h, 1000, fr.Mode.FP32_FAST, palette=pal)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_np16(counts), _np16(full))
+    np.testing.assert_array_equal(rgba.cpu().numpy(), full_rgba.cpu().numpy())
+
+
+def test_bench_exchange_branches_at_n1():
+    """bench.py --force-exchange runs the N > 1 measurements (plain gather, pipelined
+    delivery, cfg3/cfg5 row bands) over an NCCL group of one: every branch reports
+    without an `error` key (BASELINE configs[2..4])."""
+    import json
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "2",
+                        "--warmup", "3", "--no-extra", "--cpu-seconds", "0.5",
+                        "--force-exchange"], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for key in ("gather_to_rank0", "delivered_to_rank0", "bands"):
+        assert key in line, key
+    assert "error" not in line["gather_to_rank0"], line["gather_to_rank0"]
+    assert "error" not in line["delivered_to_rank0"], line["delivered_to_rank0"]
+    for name in ("cfg3", "cfg5"):
+        assert "error" not in line["bands"][name], line["bands"][name]
+    assert line["bands"]["cfg3"]["colour"] == "fused classic palette"
