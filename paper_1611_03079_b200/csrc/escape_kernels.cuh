@@ -859,6 +859,9 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
 // amortised over the group), one frame at a time.
 // ----------------------------------------------------------------------------------
 constexpr int kTileWX = 64;
+#ifndef FR_SX_K  // vote block of kernel SX (A/B knob)
+#define FR_SX_K 4
+#endif
 template <int NC, int ES, bool COLOR>
 __global__ void __launch_bounds__(kThreads)
 escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, int frame0,
@@ -876,7 +879,7 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
   const float re1 = to_state<float, false>(pixel_re(g, min(px + 1, g.W - 1)));
   const float im = to_state<float, false>(pixel_im(g, global_row(g, min(ly, g.rows - 1))));
   const int max_iter = g.max_iter;
-  const int kfull = max_iter - max_iter % 4;
+  const int kfull = max_iter - max_iter % FR_SX_K;
   const int f0 = grp * fpc;
   const int f1 = min(f0 + fpc, n_frames);
   const int64_t stride = g.frame_stride;
@@ -895,8 +898,8 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
     unsigned alive = in0 ? 1u : 0u, alive2 = in1 ? 1u : 0u;
     int cnt = 0, cnt2 = 0;
     const float cr = cs.re[f], ci = cs.im[f];
-    int n = fast_vote_loop2x_f32<4>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr, ci,
-                                    kfull);
+    int n = fast_vote_loop2x_f32<FR_SX_K>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr,
+                                          ci, kfull);
     if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
       for (; n < max_iter; ++n) {
         Iter<float, false>::step(x, y, cr, ci, alive, cnt);
