@@ -13,6 +13,10 @@
 //                             checkpointed sub-blocks, exact replay of one sub-block)
 //   escape_refill_kernel  R / A  persistent lane refill over pixel chunks; A amortises
 //                             the escape test (block-end test + exact replay)
+//   escape_pathx_kernel   SX  C-path frames, FP32_FAST: two x-adjacent pixels per lane
+//                             (packed FFMA2 loop), whole-sector count stores
+//   escape_cont2s_kernel  P2S experimental packed P2 (two orbits per lane), with the
+//   escape_replay_kernel  P3  replay kernel for its exact escape indices (off by default)
 //   colorize_kernel           count -> RGBA colour levels (HBM-bound)
 // All iteration goes through Iter<T, STRICT>::step / core or the PTX vote loops, which
 // implement the same operation sequences (FAST: doubled state, FMA-contracted; STRICT:
@@ -341,8 +345,8 @@ __device__ __forceinline__ uchar4 colour_of(const uchar4* spal, const Palette& p
   return spal[c - q * p.n];
 }
 
-// What the kernels that read colours from the device copy need of a palette (S2, P1,
-// P2X, P3): 24 bytes of kernel parameters instead of the 1.1-KB Palette (the launch
+// What the kernels that read colours from the device copy need of a palette (S2, SX,
+// P1, P2S, P3): 24 bytes of kernel parameters instead of the 1.1-KB Palette (the launch
 // copies every parameter byte; it matters for small frames).
 struct PalRef {
   const uchar4* dev;
@@ -860,7 +864,7 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
 // ----------------------------------------------------------------------------------
 constexpr int kTileWX = 64;
 #ifndef FR_SX_K  // vote block of kernel SX (A/B knob)
-#define FR_SX_K 4
+#define FR_SX_K 2  // same box: 2.629 vs 2.734 ms per bench step (profiles/r02/ab_sx_votek.txt)
 #endif
 template <int NC, int ES, bool COLOR>
 __global__ void __launch_bounds__(kThreads)
@@ -1022,8 +1026,9 @@ __device__ __forceinline__ unsigned long long global_ns() {
 //       warps take 32 items per atomic, the next grab prefetched.  The orbit continues
 //       from Z_B with the same arithmetic, so counts are bit-identical to one pass.
 // ----------------------------------------------------------------------------------
+// 16-byte aligned for binary32 so a whole item moves in one 128-bit load / store
 template <class T>
-struct QItem {
+struct alignas(sizeof(T) == 4 ? 16 : 8) QItem {
   T x, y;        // state after the phase-1 budget (kernel representation)
   int cnt;       // iterations done (= the budget)
   unsigned idx;  // pixel index row * W + px within the call's rows
@@ -1036,9 +1041,9 @@ struct ContQueue {
   unsigned pad1[31];
   unsigned done_warps;
   unsigned pad2[31];
-  unsigned left;  // P2X: orbits handed over to the leftover launch (after the tail)
+  unsigned left;  // reserved (0)
   unsigned pad3[31];
-  unsigned head2;  // P2X leftover launch: items taken
+  unsigned head2;  // reserved (0)
   unsigned pad4[31];
 };
 
@@ -1448,305 +1453,34 @@ escape_cont_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Co
   }
 }
 
-// ----------------------------------------------------------------------------------
-// P2 for FP32_FAST under the escape-monotonicity precondition (|C| <= 1.989, host-
-// checked), packed: "P2X" (escape_cont2_kernel) + "P3" (replay_kernel).
-//
-// Each lane runs TWO orbits ("slots" a and b) as the halves of packed float2 registers,
-// so every iteration is 4 FFMA2/FMUL2 for both (the FMA pipe is the bound; the block-end
-// bookkeeping issues on the ALU pipe in between).  Blocks of K bare iterations end with
-// one |Z|^2 test per slot; a finished slot
-//   * (limit reached, end state inside) stores count = max_iter directly: by
-//     monotonicity no earlier state escaped;
-//   * (end state escaped) writes a replay record -- the block's start state and its
-//     iteration index -- over its own (already consumed) queue item, and the exact
-//     escape index is recovered later by P3, one record per thread (SIMT-efficient),
-//     instead of stalling the warp here;
-// and immediately takes the next item from a per-warp ring of queue items in shared
-// memory (refilled 32 items per atomic, so a finished slot never waits for a warp-wide
-// service threshold).  Lanes idle only once the queue is dry.
-// Counts are bit-identical to the FAST oracle: the same doubled FMA sequence (packed
-// halves are separately rounded fused operations), and P3 replays with the
-// per-iteration test of that sequence.
-// ----------------------------------------------------------------------------------
-constexpr int kRing = 128;  // queue items buffered per warp (shared memory; <= 96 live)
-
+// Packed-float helpers (sm_100 FFMA2 / FMUL2: two separately rounded operations).
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ float2 fneg2(float2 a) { return make_float2(-a.x, -a.y); }
 
-// Slot life cycle.  A slot runs its orbit in blocks of K = NS sub-blocks of KS bare
-// iterations; the start state of every sub-block is kept (registers), so a slot whose
-// block end escaped records the start of the FIRST sub-block whose end escaped (by
-// monotonicity the later ones escaped too): P3 then replays at most KS steps.  A
-// finished slot takes its next orbit from its private stash (registers; no warp-
-// collective step); the warp refills empty stashes from its ring only when at least
-// kStashLow of them are empty or a slot went idle, and the ring from the queue in
-// prefetched grabs of 32.
-// phase 0: the survivors [0, tail) of P1.  Once the queue is dry a warp keeps running
-//   until it holds at most `donate` orbits, then appends those (current state, queue slot
-//   of their record) after the tail -- items[tail + left ...] -- marks their old record
-//   slots "nothing to replay" and exits, so the long drain of nearly empty warps is cut
-//   short (donate = 0: run to the end).
-// phase 1: the leftover launch over [tail, tail + left): the handed-over orbits packed
-//   densely into few warps, run to the end.
-constexpr int kStashLow = 16;
-
+// ----------------------------------------------------------------------------------
+// "P2S" (experimental, FRACTAL_P2S=1): P2 for FP32_FAST under the
+// escape-monotonicity precondition with two orbits ("slots") per lane in packed float2
+// registers (FFMA2/FMUL2), blocks of K bare iterations with the sub-block start states
+// kept and one |Z|^2 test per slot at the block end.  On cfg3's survivors the 64 slots
+// of a warp finish ~8 times per 32-iteration block, so finishing must be cheap and
+// mostly non-collective:
+//   * a finished slot writes its replay record (the start of its escaping sub-block and
+//     its index; "nothing to replay" for the iteration limit) over its consumed queue
+//     item, and continues with its stash, an item already in registers;
+//   * the emptied stashes are refilled by plain per-lane loads at ranked positions of a
+//     warp-private range of queue positions (reserved 128 at a time by one atomic, the
+//     next range reserved ahead), so the load latency is hidden by the orbit it stands
+//     behind (hundreds of iterations) -- no shared memory, no shuffles.
+// P3 (escape_replay_kernel) recovers the exact escape indices afterwards.
+// ----------------------------------------------------------------------------------
 template <bool MANDEL, bool COLOR, int K>
 __global__ void __launch_bounds__(kThreads)
-escape_cont2_kernel(const Geom g, const PalRef pal, const float jcr2, const float jci2,
-                    ContQueue* q, QItem<float>* items, int phase, int donate) {
-  constexpr int KS = 8, NS = K / KS;
-  static_assert(K % KS == 0 && NS >= 1 && NS <= 4, "blocks of 1..4 sub-blocks of 8");
-  __shared__ QItem<float> ring[kThreads / 32][kRing];
-  __shared__ unsigned ringq[kThreads / 32][kRing];  // queue position of each ring entry
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  const int max_iter = g.max_iter;
-  const unsigned tail = *reinterpret_cast<volatile unsigned*>(&q->tail);
-  const unsigned lo = phase == 0 ? 0u : tail;
-  const unsigned hi = phase == 0 ? tail : tail + *reinterpret_cast<volatile unsigned*>(&q->left);
-  unsigned* headp = phase == 0 ? &q->head : &q->head2;
-  unsigned long long* trace = g_refill_trace;
-  const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + warp;
-  if (trace && lane == 0 && phase == 0) trace[gw * 3] = global_ns();
-  QItem<float>* rg = ring[warp];
-  unsigned* rq = ringq[warp];
-  unsigned rhead = 0u, rcount = 0u;  // warp-uniform ring state
-  bool exhausted = false;            // no queue items left beyond the ring
-  unsigned pf_base = 0u;             // prefetched grab: base (lane 0 until loaded)
-  bool pf_valid = false, pf_loaded = false;
-  QItem<float> pf_item{};
-  auto reserve = [&]() {
-    if (lane == 0) pf_base = lo + atomicAdd(headp, 32u);
-    pf_valid = true;
-    pf_loaded = false;
-  };
-  auto load = [&]() {
-    const unsigned base = __shfl_sync(kFull, pf_base, 0);
-    pf_base = base;
-    const unsigned i = base + (unsigned)lane;
-    if (i < hi) pf_item = items[i];
-    pf_loaded = true;
-  };
-  auto commit = [&]() {  // the prefetched grab into the ring; reserve the next one
-    if (!pf_loaded) load();
-    const unsigned base = pf_base;
-    pf_valid = false;
-    if (base < hi) {
-      const unsigned slot = (rhead + rcount + (unsigned)lane) & (kRing - 1);
-      if (base + (unsigned)lane < hi) {
-        rg[slot] = pf_item;
-        rq[slot] = base + (unsigned)lane;
-      }
-      rcount += min(32u, hi - base);
-      __syncwarp();
-    }
-    if (base + 32u < hi) {
-      reserve();
-    } else {
-      exhausted = true;
-      if (trace && lane == 0 && phase == 0) trace[gw * 3 + 1] = global_ns();
-    }
-  };
-  auto take = [&](unsigned r, float& x, float& y, int& c, unsigned& idx, unsigned& qp) {
-    const unsigned s = (rhead + r) & (kRing - 1);
-    const QItem<float> it = rg[s];
-    x = it.x;
-    y = it.y;
-    c = it.cnt;
-    idx = it.idx;
-    qp = rq[s];
-  };
-  auto c_of = [&](unsigned idx, float& cr, float& ci) {  // MANDEL: C from the pixel
-    const int row = (int)(idx / (unsigned)g.W);
-    const int px = (int)(idx - (unsigned)row * (unsigned)g.W);
-    cr = to_state<float, false>(pixel_re(g, px));
-    ci = to_state<float, false>(pixel_im(g, global_row(g, row)));
-  };
-
-  // running slots (.x = slot a, .y = slot b) and their stashes
-  float2 X = make_float2(0.f, 0.f), Y = X;
-  float2 CR = make_float2(jcr2, jcr2), CI = make_float2(jci2, jci2);
-  int ca = 0, cb = 0;
-  unsigned ia = 0u, ib = 0u, qa = 0u, qb = 0u;
-  bool ha = false, hb = false;
-  float sxa = 0.f, sya = 0.f, sxb = 0.f, syb = 0.f;
-  int sca = 0, scb = 0;
-  unsigned sia = 0u, sib = 0u, sqa = 0u, sqb = 0u;
-  bool va = false, vb = false;  // stash valid
-  // fill the empty stashes from the ring (topping the ring up from the queue)
-  auto refill_stashes = [&]() {
-    const unsigned ea_m = __ballot_sync(kFull, !va), eb_m = __ballot_sync(kFull, !vb);
-    const unsigned need = (unsigned)(__popc(ea_m) + __popc(eb_m));
-    while (rcount < need && !exhausted) commit();
-    const unsigned ra = (unsigned)__popc(ea_m & lt);
-    const unsigned rb = (unsigned)__popc(ea_m) + (unsigned)__popc(eb_m & lt);
-    if (!va && ra < rcount) {
-      take(ra, sxa, sya, sca, sia, sqa);
-      va = true;
-    }
-    if (!vb && rb < rcount) {
-      take(rb, sxb, syb, scb, sib, sqb);
-      vb = true;
-    }
-    const unsigned used = min(need, rcount);
-    rhead = (rhead + used) & (kRing - 1);
-    rcount -= used;
-    __syncwarp();
-    if (rcount < 32u && !exhausted) commit();
-  };
-  // a free slot takes its stash
-  auto pull = [&]() {
-    if (!ha && va) {
-      X.x = sxa;
-      Y.x = sya;
-      ca = sca;
-      ia = sia;
-      qa = sqa;
-      if (MANDEL) c_of(ia, CR.x, CI.x);
-      ha = true;
-      va = false;
-    }
-    if (!hb && vb) {
-      X.y = sxb;
-      Y.y = syb;
-      cb = scb;
-      ib = sib;
-      qb = sqb;
-      if (MANDEL) c_of(ib, CR.y, CI.y);
-      hb = true;
-      vb = false;
-    }
-  };
-  reserve();
-  commit();
-  refill_stashes();
-  pull();
-  refill_stashes();
-  const float2 HALF = make_float2(0.5f, 0.5f);
-  for (;;) {
-    const unsigned hm = __ballot_sync(kFull, ha), hbm = __ballot_sync(kFull, hb);
-    if ((hm | hbm) == 0u) break;
-    if (exhausted && rcount == 0u && donate > 0 && !__any_sync(kFull, va || vb) &&
-        __popc(hm) + __popc(hbm) <= donate) {
-      // hand the held orbits to the leftover launch and leave
-      const unsigned n = (unsigned)(__popc(hm) + __popc(hbm));
-      unsigned base = 0u;
-      if (lane == 0) base = atomicAdd(&q->left, n);
-      base = tail + __shfl_sync(kFull, base, 0);
-      const unsigned ra = (unsigned)__popc(hm & lt);
-      const unsigned rb = (unsigned)__popc(hm) + (unsigned)__popc(hbm & lt);
-      QItem<float> skip;
-      skip.x = 0.f;
-      skip.y = 0.f;
-      skip.cnt = -1;
-      if (ha) {
-        QItem<float> it;
-        it.x = X.x; it.y = Y.x; it.cnt = ca; it.idx = ia;
-        items[base + ra] = it;
-        skip.idx = ia;
-        items[qa] = skip;
-      }
-      if (hb) {
-        QItem<float> it;
-        it.x = X.y; it.y = Y.y; it.cnt = cb; it.idx = ib;
-        items[base + rb] = it;
-        skip.idx = ib;
-        items[qb] = skip;
-      }
-      break;
-    }
-    float2 CX[NS], CY[NS];  // start state of each sub-block
-#pragma unroll
-    for (int sb = 0; sb < NS; ++sb) {
-      CX[sb] = X;
-      CY[sb] = Y;
-#pragma unroll
-      for (int j = 0; j < KS; ++j) {
-        const float2 YY = fmul2(Y, Y);
-        const float2 T = ffma2(X, X, fneg2(YY));
-        const float2 Yn = ffma2(X, Y, CI);
-        X = ffma2(T, HALF, CR);
-        Y = Yn;
-      }
-    }
-    const float2 M = ffma2(X, X, fmul2(Y, Y));
-    const bool ea = !(M.x <= 16.0f), eb = !(M.y <= 16.0f);  // unordered: NaN/inf escaped
-    const bool fa = ha && (ea || ca + K >= max_iter);
-    const bool fb = hb && (eb || cb + K >= max_iter);
-    if (pf_valid && !pf_loaded) load();  // stage the prefetched grab meanwhile
-    if (__any_sync(kFull, fa || fb)) {
-      // the escaping sub-block: the first whose end state (the next start) escaped
-      float xa = CX[NS - 1].x, ya = CY[NS - 1].x, xb = CX[NS - 1].y, yb = CY[NS - 1].y;
-      int oa = (NS - 1) * KS, ob = (NS - 1) * KS;
-#pragma unroll
-      for (int sb = NS - 2; sb >= 0; --sb) {
-        const float2 m = ffma2(CX[sb + 1], CX[sb + 1], fmul2(CY[sb + 1], CY[sb + 1]));
-        if (!(m.x <= 16.0f)) {
-          xa = CX[sb].x; ya = CY[sb].x; oa = sb * KS;
-        }
-        if (!(m.y <= 16.0f)) {
-          xb = CX[sb].y; yb = CY[sb].y; ob = sb * KS;
-        }
-      }
-      if (fa) {
-        QItem<float> r;
-        r.x = xa; r.y = ya; r.cnt = ea ? ca + oa : -1; r.idx = ia;
-        items[qa] = r;
-        if (!ea) {
-          g.counts[ia] = (uint16_t)max_iter;
-          if (COLOR) g.rgba[ia] = pal.interior;
-        }
-      }
-      if (fb) {
-        QItem<float> r;
-        r.x = xb; r.y = yb; r.cnt = eb ? cb + ob : -1; r.idx = ib;
-        items[qb] = r;
-        if (!eb) {
-          g.counts[ib] = (uint16_t)max_iter;
-          if (COLOR) g.rgba[ib] = pal.interior;
-        }
-      }
-      if (fa) ha = false;
-      if (fb) hb = false;
-      pull();
-    }
-    if (ha && !fa) ca += K;
-    if (hb && !fb) cb += K;
-    // refill the stashes when enough are empty, or a slot is idle with orbits left
-    const unsigned empty = (unsigned)(__popc(__ballot_sync(kFull, !va)) +
-                                      __popc(__ballot_sync(kFull, !vb)));
-    if (empty >= (unsigned)kStashLow && (rcount > 0u || !exhausted)) {
-      refill_stashes();
-      pull();
-    } else if (__any_sync(kFull, !ha || !hb) && (rcount > 0u || !exhausted)) {
-      refill_stashes();
-      pull();
-    }
-  }
-  if (trace && lane == 0 && phase == 0) trace[gw * 3 + 2] = global_ns();
-}
-
-// ----------------------------------------------------------------------------------
-// "P2T": the one-orbit amortised P2 (escape_cont_kernel<..., AMORT>) in packed form, for
-// FP32_FAST under the escape-monotonicity precondition.  Each lane runs two orbits
-// (slots a, b) as the halves of float2 registers (FFMA2/FMUL2).  Blocks of K = NS x KS
-// bare iterations with the sub-block start states kept; at a block end a slot whose
-// end state escaped (or that reached the iteration limit) notes the start of its
-// escaping sub-block and FREEZES (done).  When at least TH of the warp's 64 slots are
-// done (all of them once the queue is dry), the warp services them together: one packed
-// replay of <= KS steps with the per-iteration test recovers every exact escape index,
-// the counts (and colours) are stored, and the freed slots are refilled from the staged
-// grab of 32 queue items (next grab prefetched, as in the one-orbit P2).
-// ----------------------------------------------------------------------------------
-template <bool MANDEL, bool COLOR, int K, int TH>
-__global__ void __launch_bounds__(kThreads)
-escape_cont2t_kernel(const Geom g, const PalRef pal, const float jcr2, const float jci2,
-                     ContQueue* q, const QItem<float>* items) {
+escape_cont2s_kernel(const Geom g, const PalRef pal, const float jcr2, const float jci2,
+                     ContQueue* q, QItem<float>* items) {
   constexpr int KS = 8, NS = K / KS;
   static_assert(K % KS == 0 && NS >= 1 && NS <= 8, "blocks of sub-blocks of 8");
+  constexpr unsigned RG = 128;  // queue positions per range reservation
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const int max_iter = g.max_iter;
@@ -1754,96 +1488,62 @@ escape_cont2t_kernel(const Geom g, const PalRef pal, const float jcr2, const flo
   unsigned long long* trace = g_refill_trace;
   const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   if (trace && lane == 0) trace[gw * 3] = global_ns();
-  // staged grabs of 32 queue items (one per lane), as in escape_cont_kernel
-  bool exhausted = false;
-  unsigned cbase = 0u, gpos = 0u, gend = 0u;
-  QItem<float> cur{}, nxt{};
-  unsigned nbase = 0u, pf = 0u;
-  bool nxt_loaded = false, pf_issued = false;
-  auto load_grab = [&](unsigned base, QItem<float>& dst) {
-    if (base + (unsigned)lane < n_items) dst = items[base + (unsigned)lane];
-  };
-  // slots (.x = a, .y = b)
-  float2 X = make_float2(0.f, 0.f), Y = X;
-  float2 CR = make_float2(jcr2, jcr2), CI = make_float2(jci2, jci2);
-  int ca = 0, cb = 0;                    // iterations done before the current block
-  unsigned ia = 0u, ib = 0u;             // pixel index
-  bool ha = false, hb = false;           // holds an orbit
-  bool da = false, db = false;           // finished, awaiting service
-  bool ea = false, eb = false;           // finished by escape (else: iteration limit)
-  float2 RX = X, RY = X;                 // replay start (escaping sub-block)
-  int ra = 0, rb = 0;                    // its iteration index
   auto c_of = [&](unsigned idx, float& cr, float& ci) {
     const int row = (int)(idx / (unsigned)g.W);
     const int px = (int)(idx - (unsigned)row * (unsigned)g.W);
     cr = to_state<float, false>(pixel_re(g, px));
     ci = to_state<float, false>(pixel_im(g, global_row(g, row)));
   };
-  // give every free slot an item (slots a first, then b), fetching grabs as needed
-  auto dispense = [&]() {
-    unsigned na = __ballot_sync(kFull, !ha), nb = __ballot_sync(kFull, !hb);
-    while ((na | nb) != 0u && !exhausted) {
-      if (gpos >= gend) {
-        if (!nxt_loaded) {
-          unsigned base = 0u;
-          if (lane == 0) base = pf_issued ? pf : atomicAdd(&q->head, 32u);
-          nbase = __shfl_sync(kFull, base, 0);
-          pf_issued = false;
-          if (nbase < n_items) load_grab(nbase, nxt);
-        }
-        nxt_loaded = false;
-        if (nbase >= n_items) {
-          exhausted = true;
-          if (trace && lane == 0) trace[gw * 3 + 1] = global_ns();
-          break;
-        }
-        cur = nxt;
-        cbase = nbase;
-        gpos = nbase;
-        gend = min(nbase + 32u, n_items);
-        if (gend < n_items) {
-          if (lane == 0) pf = atomicAdd(&q->head, 32u);
-          pf_issued = true;
-        }
-      }
-      const unsigned avail = gend - gpos;
-      const unsigned rka = (unsigned)__popc(na & lt);
-      const unsigned rkb = (unsigned)__popc(na) + (unsigned)__popc(nb & lt);
-      const bool wa = ((na >> lane) & 1u) && rka < avail;
-      const bool wb = ((nb >> lane) & 1u) && rkb < avail;
-      const int sa = (int)(gpos - cbase + (rka < avail ? rka : 0u));
-      const int sb = (int)(gpos - cbase + (rkb < avail ? rkb : 0u));
-      const float xa_ = __shfl_sync(kFull, cur.x, sa), ya_ = __shfl_sync(kFull, cur.y, sa);
-      const int ka_ = __shfl_sync(kFull, cur.cnt, sa);
-      const unsigned ja_ = __shfl_sync(kFull, cur.idx, sa);
-      const float xb_ = __shfl_sync(kFull, cur.x, sb), yb_ = __shfl_sync(kFull, cur.y, sb);
-      const int kb_ = __shfl_sync(kFull, cur.cnt, sb);
-      const unsigned jb_ = __shfl_sync(kFull, cur.idx, sb);
-      if (wa) {
-        X.x = xa_; Y.x = ya_; ca = ka_; ia = ja_; ha = true;
-        if (MANDEL) c_of(ia, CR.x, CI.x);
-      }
-      if (wb) {
-        X.y = xb_; Y.y = yb_; cb = kb_; ib = jb_; hb = true;
-        if (MANDEL) c_of(ib, CR.y, CI.y);
-      }
-      const unsigned want = (unsigned)(__popc(na) + __popc(nb));
-      gpos += want < avail ? want : avail;
-      na = __ballot_sync(kFull, !ha);
-      nb = __ballot_sync(kFull, !hb);
-      if (!pf_issued || nxt_loaded || gpos >= gend) continue;
-      // the prefetch atomic has had a dispense round to return: stage its items
-      nbase = __shfl_sync(kFull, pf, 0);
-      pf_issued = false;
-      nxt_loaded = true;
-      if (nbase < n_items) load_grab(nbase, nxt);
+  // ---- warp-private queue ranges: current [r0, r1), next [nx, nx + RG) (reserved)
+  unsigned r0 = 0u, r1 = 0u, nx = 0u;
+  bool exhausted = false;
+  {
+    unsigned b = 0u;
+    if (lane == 0) b = atomicAdd(&q->head, RG);
+    r0 = __shfl_sync(kFull, b, 0);
+    r1 = r0 + RG;
+    if (lane == 0) nx = atomicAdd(&q->head, RG);  // lane 0 only, until shuffled
+  }
+  // slots and stashes: the first 128 positions of the range, in that order
+  float2 X, Y;
+  float2 CR = make_float2(jcr2, jcr2), CI = make_float2(jci2, jci2);
+  int ca, cb;
+  unsigned ia, ib, qa, qb;
+  bool ha, hb;
+  QItem<float> sa{}, sb{};
+  unsigned sqa = 0u, sqb = 0u;
+  bool va, vb;
+  {
+    const unsigned pa = r0 + (unsigned)lane, pb = pa + 32u, psa = pa + 64u, psb = pa + 96u;
+    QItem<float> ta{}, tb{};
+    ha = pa < n_items;
+    hb = pb < n_items;
+    va = psa < n_items;
+    vb = psb < n_items;
+    if (ha) ta = items[pa];
+    if (hb) tb = items[pb];
+    if (va) sa = items[psa];
+    if (vb) sb = items[psb];
+    sqa = psa;
+    sqb = psb;
+    X = make_float2(ta.x, tb.x);
+    Y = make_float2(ta.y, tb.y);
+    ca = ta.cnt;
+    cb = tb.cnt;
+    ia = ta.idx;
+    ib = tb.idx;
+    qa = pa;
+    qb = pb;
+    if (MANDEL) {
+      if (ha) c_of(ia, CR.x, CI.x);
+      if (hb) c_of(ib, CR.y, CI.y);
     }
-  };
-  dispense();
+    r0 = r1;  // the first range is used up
+    exhausted = r0 >= n_items && __shfl_sync(kFull, nx, 0) >= n_items;
+  }
   const float2 HALF = make_float2(0.5f, 0.5f);
   for (;;) {
-    const int n_held = __popc(__ballot_sync(kFull, ha)) + __popc(__ballot_sync(kFull, hb));
-    if (n_held == 0) break;
+    if (!__any_sync(kFull, ha || hb)) break;
     float2 CX[NS], CY[NS];
 #pragma unroll
     for (int s2 = 0; s2 < NS; ++s2) {
@@ -1859,11 +1559,14 @@ escape_cont2t_kernel(const Geom g, const PalRef pal, const float jcr2, const flo
       }
     }
     const float2 M = ffma2(X, X, fmul2(Y, Y));
-    const bool xa = !(M.x <= 16.0f), xb = !(M.y <= 16.0f);  // unordered: NaN/inf escaped
-    const bool fa = ha && !da && (xa || ca + K >= max_iter);
-    const bool fb = hb && !db && (xb || cb + K >= max_iter);
-    if (__any_sync(kFull, fa || fb)) {
-      // escaping sub-block = the first whose end state (the next start) escaped
+    const bool ea = !(M.x <= 16.0f), eb = !(M.y <= 16.0f);  // unordered: NaN/inf escaped
+    const bool fa = ha && (ea || ca + K >= max_iter);
+    const bool fb = hb && (eb || cb + K >= max_iter);
+    if (ha && !fa) ca += K;
+    if (hb && !fb) cb += K;
+    if (!__any_sync(kFull, fa || fb)) continue;
+    // ---- finished slots: replay record (or the interior count) over the consumed item
+    {
       float2 sx = CX[NS - 1], sy = CY[NS - 1];
       int oa = (NS - 1) * KS, ob = (NS - 1) * KS;
 #pragma unroll
@@ -1872,69 +1575,69 @@ escape_cont2t_kernel(const Geom g, const PalRef pal, const float jcr2, const flo
         if (!(m.x <= 16.0f)) { sx.x = CX[s2].x; sy.x = CY[s2].x; oa = s2 * KS; }
         if (!(m.y <= 16.0f)) { sx.y = CX[s2].y; sy.y = CY[s2].y; ob = s2 * KS; }
       }
-      if (fa) { RX.x = sx.x; RY.x = sy.x; ra = ca + oa; ea = xa; da = true; }
-      if (fb) { RX.y = sx.y; RY.y = sy.y; rb = cb + ob; eb = xb; db = true; }
-    }
-    if (ha && !da) ca += K;
-    if (hb && !db) cb += K;
-    const int n_done = __popc(__ballot_sync(kFull, da)) + __popc(__ballot_sync(kFull, db));
-    const int thr = exhausted ? n_held : (TH < n_held ? TH : n_held);
-    if (n_done < thr || n_done == 0) continue;
-    // ---- service: packed replay of the escaped slots, stores, refill
-    {
-      bool pa = da && ea, pb = db && eb;  // still searching
-      int na_ = 0, nb_ = 0;
-      float2 x = RX, y = RY;
-#pragma unroll 1
-      for (int j = 0; j <= KS; ++j) {
-        if (!__any_sync(kFull, pa || pb)) break;
-        const float2 m = ffma2(x, x, fmul2(y, y));
-        pa = pa && (m.x <= 16.0f);
-        pb = pb && (m.y <= 16.0f);
-        if (pa) ++na_;
-        if (pb) ++nb_;
-        const float2 YY = fmul2(y, y);
-        const float2 T = ffma2(x, x, fneg2(YY));
-        const float2 Yn = ffma2(x, y, CI);
-        x = ffma2(T, HALF, CR);
-        y = Yn;
+      if (fa) {
+        QItem<float> r;
+        r.x = sx.x; r.y = sy.x; r.cnt = ea ? ca + oa : -1; r.idx = ia;
+        items[qa] = r;
+        if (!ea) {
+          g.counts[ia] = (uint16_t)max_iter;
+          if (COLOR) g.rgba[ia] = pal.interior;
+        }
+        // continue with the stash
+        X.x = sa.x; Y.x = sa.y; ca = sa.cnt; ia = sa.idx; qa = sqa;
+        ha = va;
+        va = false;
+        if (MANDEL && ha) c_of(ia, CR.x, CI.x);
       }
-      if (da) {
-        const int c0 = ea ? ra + na_ : max_iter;
-        const int count = c0 < max_iter ? c0 : max_iter;
-        g.counts[ia] = (uint16_t)count;
-        if (COLOR) g.rgba[ia] = colour_dev(pal, count, max_iter);
-        ha = false;
-        da = false;
-      }
-      if (db) {
-        const int c0 = eb ? rb + nb_ : max_iter;
-        const int count = c0 < max_iter ? c0 : max_iter;
-        g.counts[ib] = (uint16_t)count;
-        if (COLOR) g.rgba[ib] = colour_dev(pal, count, max_iter);
-        hb = false;
-        db = false;
+      if (fb) {
+        QItem<float> r;
+        r.x = sx.y; r.y = sy.y; r.cnt = eb ? cb + ob : -1; r.idx = ib;
+        items[qb] = r;
+        if (!eb) {
+          g.counts[ib] = (uint16_t)max_iter;
+          if (COLOR) g.rgba[ib] = pal.interior;
+        }
+        X.y = sb.x; Y.y = sb.y; cb = sb.cnt; ib = sb.idx; qb = sqb;
+        hb = vb;
+        vb = false;
+        if (MANDEL && hb) c_of(ib, CR.y, CI.y);
       }
     }
-    dispense();
+    if (exhausted) continue;
+    // ---- refill the emptied stashes from the warp's ranges (per-lane loads)
+    const unsigned ma = __ballot_sync(kFull, fa), mb = __ballot_sync(kFull, fb);
+    const unsigned m = (unsigned)(__popc(ma) + __popc(mb));
+    const unsigned ka = (unsigned)__popc(ma & lt);
+    const unsigned kb = (unsigned)__popc(ma) + (unsigned)__popc(mb & lt);
+    const unsigned cur = r1 - r0;  // positions left in the current range
+    const unsigned nb = __shfl_sync(kFull, nx, 0);
+    auto pos_of = [&](unsigned k) { return k < cur ? r0 + k : nb + (k - cur); };
+    if (fa) {
+      sqa = pos_of(ka);
+      va = sqa < n_items;
+      if (va) sa = items[sqa];
+    }
+    if (fb) {
+      sqb = pos_of(kb);
+      vb = sqb < n_items;
+      if (vb) sb = items[sqb];
+    }
+    if (m < cur) {
+      r0 += m;
+    } else {  // moved into the next range: reserve the one after it
+      r0 = nb + (m - cur);
+      r1 = nb + RG;
+      if (lane == 0) nx = atomicAdd(&q->head, RG);
+      if (nb >= n_items) {
+        exhausted = true;
+        if (trace && lane == 0) trace[gw * 3 + 1] = global_ns();
+      }
+    }
   }
   if (trace && lane == 0) trace[gw * 3 + 2] = global_ns();
-  // ---- self-reset of the queue by the last warp to finish
-  if (lane == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(&q->done_warps, 1u);
-    if (prev == gridDim.x * (kThreads / 32) - 1) {
-      q->tail = 0u;
-      q->head = 0u;
-      q->left = 0u;
-      q->head2 = 0u;
-      q->done_warps = 0u;
-      __threadfence();
-    }
-  }
 }
 
-// P3: exact escape index of P2X's replay records, one record per thread: the FAST step
+// P3: exact escape index of P2S's replay records, one record per thread: the FAST step
 // with the per-iteration test from the recorded block-start state Z_cnt (the record's
 // block escaped at its end state, so the loop ends within K steps).  Resets the queue
 // header when the last CTA finishes (the next call's P1 appends from 0).

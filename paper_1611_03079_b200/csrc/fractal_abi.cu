@@ -221,14 +221,17 @@ cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr:
     if (sx) {
       fr::Geom gx = g;
       gx.tiles_x = (g.W + fr::kTileWX - 1) / fr::kTileWX;
+      // 64 frames per CTA (bench: 16/32/64/128 -> 2.80/2.73/2.70/2.72 ms,
+      // profiles/r02/ab_sx_fpc.txt); FRACTAL_FPC overrides
+      const int fpcx = fpc_env > 0 ? fpc : (n_frames < 64 ? n_frames : 64);
       const dim3 gridx =
-          tile_grid(gx, (g.rows + fr::kTileH - 1) / fr::kTileH, (n_frames + fpc - 1) / fpc);
+          tile_grid(gx, (g.rows + fr::kTileH - 1) / fr::kTileH, (n_frames + fpcx - 1) / fpcx);
       if (g.counts8 != nullptr)
         fr::escape_pathx_kernel<NC, 1, COLOR>
-            <<<gridx, fr::kThreads, 0, s>>>(gx, pal_ref(pal), cs, frame0, n_frames, fpc);
+            <<<gridx, fr::kThreads, 0, s>>>(gx, pal_ref(pal), cs, frame0, n_frames, fpcx);
       else
         fr::escape_pathx_kernel<NC, 2, COLOR>
-            <<<gridx, fr::kThreads, 0, s>>>(gx, pal_ref(pal), cs, frame0, n_frames, fpc);
+            <<<gridx, fr::kThreads, 0, s>>>(gx, pal_ref(pal), cs, frame0, n_frames, fpcx);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return cudaGetLastError();
     }
@@ -447,15 +450,11 @@ int twophase_budget(bool amort, bool f64) {
   return v < 4 ? 4 : v - v % 4;
 }
 
-bool p2t_on() {
-  static const bool v = env_int("FRACTAL_P2T", 0) != 0;  // off: slower
+bool p2s_on() {  // experimental packed P2: off, slower than the one-orbit P2
+  static const bool v = env_int("FRACTAL_P2S", 0) != 0;
   return v;
 }
 
-bool p2x_on() {
-  static const bool v = env_int("FRACTAL_P2X", 0) != 0;  // off: slower so far
-  return v;
-}
 
 #ifndef FR_P1A_KS  // amortised P1 sub-block (0 = exact per-iteration test)
 #define FR_P1A_KS 0
@@ -487,8 +486,8 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   }
   auto* q = static_cast<fr::ContQueue*>(qp);
   void* ip = nullptr;
-  // (+ room for P2X's hand-over of at most 64 orbits per warp after the survivors)
-  const size_t extra = (size_t)sm_count() * 8 * (fr::kThreads / 32) * 64;
+  // (+ 128 positions per warp of the largest P2 grid: P2S reserves whole ranges)
+  const size_t extra = (size_t)sm_count() * 8 * (fr::kThreads / 32) * 128;
   e = buffer_for(g_items, s, ((size_t)n + extra) * sizeof(fr::QItem<T>), &ip);
   if (e != cudaSuccess) return e;
   auto* items = static_cast<fr::QItem<T>*>(ip);
@@ -531,54 +530,16 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  // FP32_FAST under the precondition: the packed two-slot P2 with threshold service
-  // (P2T; FRACTAL_P2T=0 falls back; FRACTAL_P2T_TH: service threshold of 64 slots)
+  // FP32_FAST under the precondition: the packed two-slot P2 with stashes (P2S) + P3
+  // (FRACTAL_P2S=0 falls back; FRACTAL_P2S_K: block 16/32/64)
   if constexpr (!STRICT && std::is_same<T, float>::value) {
-    if (amort && p2t_on()) {
-      static const int th = env_int("FRACTAL_P2T_TH", 16);
-      auto kt = fr::escape_cont2t_kernel<MANDEL, COLOR, 32, 16>;
-      if (th == 8) kt = fr::escape_cont2t_kernel<MANDEL, COLOR, 32, 8>;
-      else if (th == 24) kt = fr::escape_cont2t_kernel<MANDEL, COLOR, 32, 24>;
-      else if (th == 32) kt = fr::escape_cont2t_kernel<MANDEL, COLOR, 32, 32>;
-      else if (th == 116) kt = fr::escape_cont2t_kernel<MANDEL, COLOR, 16, 16>;
-      else if (th == 164) kt = fr::escape_cont2t_kernel<MANDEL, COLOR, 64, 16>;
-      static const int occt = [&] {
-        int o = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kt, fr::kThreads, 0) !=
-                cudaSuccess || o <= 0)
-          o = 1;
-        return o;
-      }();
-      static const int occ_env = env_int("FRACTAL_P2_OCC", 0);
-      const int want = occ_env > 0 ? occ_env : 3;
-      const int o2 = want < occt ? want : occt;
-      kt<<<(unsigned)(sm_count() * o2), fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, q,
-                                                              items);
-      e = cudaGetLastError();
-      if (e != cudaSuccess) {
-        cudaMemsetAsync(qp, 0, sizeof(fr::ContQueue), s);
-        return e;
-      }
-      g_launches.fetch_add(1, std::memory_order_relaxed);
-      return cudaSuccess;
-    }
-  }
-  // FP32_FAST under the precondition: the packed two-slot P2 (P2X) with a per-warp ring
-  // of queue items, its leftover launch for the orbits handed over by nearly empty warps
-  // once the queue is dry, then the replay kernel P3 for the exact escape indices
-  // (FRACTAL_P2X=0: the one-orbit amortised P2 below; FRACTAL_P2X_K: block 16/32;
-  // FRACTAL_P2X_D: hand-over threshold in held orbits per warp, 0 = none)
-  if constexpr (!STRICT && std::is_same<T, float>::value) {
-    if (amort && p2x_on()) {
-      static const int kx = env_int("FRACTAL_P2X_K", 32);
-      static const int dx = env_int("FRACTAL_P2X_D", 16);
-      auto k2 = fr::escape_cont2_kernel<MANDEL, COLOR, 32>;
-      auto k3 = fr::escape_replay_kernel<MANDEL, COLOR, 32>;
-      if (kx == 16) {
-        k2 = fr::escape_cont2_kernel<MANDEL, COLOR, 16>;
-        k3 = fr::escape_replay_kernel<MANDEL, COLOR, 16>;
-      }
-      static const int occx = [&] {
+    if (amort && p2s_on()) {
+      static const int ks = env_int("FRACTAL_P2S_K", 32);
+      auto k2 = fr::escape_cont2s_kernel<MANDEL, COLOR, 32>;
+      if (ks == 16) k2 = fr::escape_cont2s_kernel<MANDEL, COLOR, 16>;
+      else if (ks == 64) k2 = fr::escape_cont2s_kernel<MANDEL, COLOR, 64>;
+      auto k3 = fr::escape_replay_kernel<MANDEL, COLOR, 8>;
+      static const int occs = [&] {
         int o = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k2, fr::kThreads, 0) !=
                 cudaSuccess || o <= 0)
@@ -586,24 +547,15 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
         return o;
       }();
       static const int occ_env = env_int("FRACTAL_P2_OCC", 0);
-      const int want = occ_env > 0 ? occ_env : 2;
-      const int o2 = want < occx ? want : occx;
-      const unsigned grid0 = (unsigned)(sm_count() * o2);
-      // leftover launch: at most `dx` orbits per phase-0 warp, 64 per warp after
-      const unsigned warps1 = (grid0 * (fr::kThreads / 32) * (unsigned)dx + 63u) / 64u;
-      const unsigned grid1 = (warps1 + fr::kThreads / 32 - 1) / (fr::kThreads / 32);
-      k2<<<grid0, fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, q, items, 0, dx);
+      const int want = occ_env > 0 ? occ_env : 3;
+      const int o2 = want < occs ? want : occs;
+      k2<<<(unsigned)(sm_count() * o2), fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, q,
+                                                              items);
       e = cudaGetLastError();
       if (e == cudaSuccess) {
         g_launches.fetch_add(1, std::memory_order_relaxed);
-        if (dx > 0) {
-          k2<<<grid1 > 0 ? grid1 : 1u, fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, q, items, 1, 0);
-          e = cudaGetLastError();
-          if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
-        }
-      }
-      if (e == cudaSuccess) {
-        k3<<<(unsigned)(sm_count() * 8), fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, q, items);
+        k3<<<(unsigned)(sm_count() * 8), fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, q,
+                                                               items);
         e = cudaGetLastError();
       }
       if (e != cudaSuccess) {

@@ -97,19 +97,13 @@ def test_fast_mode_identical_across_schedulers():
                                  {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_TILES": "2"},
                                  {"FRACTAL_SCHED": "refill"}, {"FRACTAL_SCHED": "amort"},
                                  {"FRACTAL_SCHED": "static"},
-                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P2T": "0"},
-                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P2T_TH": "8",
-                                  "FRACTAL_BUDGET": "8", "FRACTAL_P2_OCC": "1"},
-                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P2T_TH": "116"},
-                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P2T_TH": "164"},
-                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P2T": "0",
-                                  "FRACTAL_P2X": "1"},
-                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P2T": "0",
-                                  "FRACTAL_P2X": "1", "FRACTAL_P2X_D": "0",
-                                  "FRACTAL_P2X_K": "16"},
-                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P2T": "0",
-                                  "FRACTAL_P2X": "1", "FRACTAL_BUDGET": "8",
-                                  "FRACTAL_P2_OCC": "1"}])
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P2S": "1"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P2S": "1",
+                                  "FRACTAL_P2S_K": "16"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P2S": "1",
+                                  "FRACTAL_P2S_K": "64"},
+                                 {"FRACTAL_SCHED": "twophase", "FRACTAL_P2S": "1",
+                                  "FRACTAL_BUDGET": "8", "FRACTAL_P2_OCC": "1"}])
 def test_fast_exact_under_forced_scheduler(env):
     """FAST counts equal the FAST oracle bit for bit under every kernel family, including
     P2 with the amortised block-end test and with the exact test."""
