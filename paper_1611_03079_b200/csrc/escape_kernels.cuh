@@ -488,9 +488,30 @@ __device__ __forceinline__ int fast_vote_loop2x_f32(float& x, float& y, int& cnt
                                                     int& cnt2, unsigned& alive2, float cr2,
                                                     float ci2, float cr2b, float ci2b,
                                                     int kfull) {
-  static_assert(K == 2 || K == 4, "vote blocks of 2 or 4");
+  static_assert(K == 1 || K == 2 || K == 4, "vote blocks of 1, 2 or 4");
   int n;
-  if constexpr (K == 4) {
+  if constexpr (K == 1) {
+    asm volatile(
+        "{\n\t.reg .pred pa, pb, pm;\n\t.reg .b64 X, Y, CR, CI, HALF, yy, m, nyy, t;\n\t"
+        ".reg .f32 m1, m2, n1, n2;\n\t"
+        "mov.b64 X, {%0, %5};\n\tmov.b64 Y, {%1, %6};\n\t"
+        "mov.b64 CR, {%12, %14};\n\tmov.b64 CI, {%13, %15};\n\t"
+        "mov.b64 HALF, {0f3F000000, 0f3F000000};\n\t"
+        "setp.ne.u32 pa, %3, 0;\n\tsetp.ne.u32 pb, %8, 0;\n\tmov.u32 %4, 0;\n\t"
+        "setp.gt.s32 pm, %9, 0;\n\t@!pm bra FR_X1B_DONE;\n"
+        "FR_X1B_LOOP:\n\t" FR_FAST_STEP2X
+        "add.s32 %4, %4, 1;\n\t"
+        "or.pred pm, pa, pb;\n\t"
+        "vote.sync.any.pred pm, pm, 0xffffffff;\n\t"
+        "setp.lt.and.s32 pm, %4, %9, pm;\n\t"
+        "@pm bra FR_X1B_LOOP;\n"
+        "FR_X1B_DONE:\n\t"
+        "mov.b64 {%0, %5}, X;\n\tmov.b64 {%1, %6}, Y;\n\t"
+        "selp.u32 %3, 1, 0, pa;\n\tselp.u32 %8, 1, 0, pb;\n\t}"
+        : "+f"(x), "+f"(y), "+r"(cnt), "+r"(alive), "=r"(n), "+f"(x2), "+f"(y2), "+r"(cnt2),
+          "+r"(alive2)
+        : "r"(kfull), "r"(0), "r"(0), "f"(cr2), "f"(ci2), "f"(cr2b), "f"(ci2b));
+  } else if constexpr (K == 4) {
     asm volatile(
         "{\n\t.reg .pred pa, pb, pm;\n\t.reg .b64 X, Y, CR, CI, HALF, yy, m, nyy, t;\n\t"
         ".reg .f32 m1, m2, n1, n2;\n\t"

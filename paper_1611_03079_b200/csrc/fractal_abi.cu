@@ -30,11 +30,13 @@ int env_int(const char* name, int dflt) {
   return e ? std::atoi(e) : dflt;
 }
 
-// Vote block of the fast fp32 two-orbit loops in S2 and P1 (FRACTAL_VOTE_K: 4 default,
-// 2 for the same-box A/B of DESIGN.md §5.1b)
+// Vote block of the fast fp32 two-orbit loops in S2 and P1 (FRACTAL_VOTE_K: 2 default
+// since the packed loop, 4 selectable).  Same box, round 2: cfg2 21.8 -> 20.6 us, cfg3
+// 0.1695 -> 0.1653 ms (profiles/r02/ab_votek_*.txt); with the scalar loop of round 1,
+// 4 was faster
 int vote_k() {
-  static const int v = env_int("FRACTAL_VOTE_K", 4);
-  return v == 2 ? 2 : 4;
+  static const int v = env_int("FRACTAL_VOTE_K", 2);
+  return v == 4 ? 4 : 2;
 }
 
 bool env_is(const char* name, const char* value) {

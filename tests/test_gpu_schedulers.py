@@ -92,7 +92,7 @@ def test_fast_mode_identical_across_schedulers():
                                   "FRACTAL_P1_PRE": "8"},
                                  {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_AMORT": "8",
                                   "FRACTAL_P1_PRE": "16"},
-                                 {"FRACTAL_VOTE_K": "2"},
+                                 {"FRACTAL_VOTE_K": "4"},
                                  {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_AMORT": "0"},
                                  {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_TILES": "2"},
                                  {"FRACTAL_SCHED": "refill"}, {"FRACTAL_SCHED": "amort"},

@@ -19,11 +19,25 @@ jr = torch.empty((1080, 1920, 4), dtype=torch.uint8, device="cuda")
 mc = torch.empty((180, 240), dtype=torch.uint16, device="cuda")
 mr = torch.empty((180, 240, 4), dtype=torch.uint8, device="cuda")
 res = {}
-for mode in (fr.Mode.FP32_FAST, fr.Mode.FP32_STRICT):
-    def tick(k):
-        fr.julia_render_ex(complex(cs[k]), jw, 1920, 1080, 100, mode, palette=pal, out=jc, out_rgba=jr)
-        fr.mandelbrot_param_map(mw, 240, 180, 100, mode, palette=pal, out=mc, out_rgba=mr)
-        torch.cuda.current_stream().synchronize()
+plans = {}
+for variant, mode in (("", fr.Mode.FP32_FAST), ("", fr.Mode.FP32_STRICT),
+                      ("plan", fr.Mode.FP32_FAST)):
+    if variant == "plan":  # arguments marshalled once (binding.FramePlan)
+        jp = fr.FramePlan("julia", jw, 1920, 1080, 100, mode, palette=pal, out=jc, out_rgba=jr)
+        mp = fr.FramePlan("mandelbrot", mw, 240, 180, 100, mode, palette=pal, out=mc,
+                          out_rgba=mr)
+        stream = torch.cuda.current_stream()
+
+        def tick(k):
+            jp.render(complex(cs[k]))
+            mp.render()
+            stream.synchronize()
+    else:
+        def tick(k):
+            fr.julia_render_ex(complex(cs[k]), jw, 1920, 1080, 100, mode, palette=pal, out=jc,
+                               out_rgba=jr)
+            fr.mandelbrot_param_map(mw, 240, 180, 100, mode, palette=pal, out=mc, out_rgba=mr)
+            torch.cuda.current_stream().synchronize()
     for k in range(10): tick(k)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(TICKS + 1)]
     import time
@@ -35,9 +49,10 @@ for mode in (fr.Mode.FP32_FAST, fr.Mode.FP32_STRICT):
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / TICKS * 1e3
     gpu = [ev[k].elapsed_time(ev[k + 1]) for k in range(TICKS)]
-    res[mode.name] = {"ms_per_tick_wall": wall, "ticks_per_s_wall": 1e3 / wall,
+    name = mode.name + ("_plan" if variant else "")
+    res[name] = {"ms_per_tick_wall": wall, "ticks_per_s_wall": 1e3 / wall,
                       "ms_per_tick_gpu_median": float(np.median(gpu)),
                       "ms_per_tick_gpu_p99": float(np.percentile(gpu, 99))}
-    print(mode.name, json.dumps(res[mode.name]), flush=True)
+    print(name, json.dumps(res[name]), flush=True)
 json.dump({"experiment": "interactive tick (P:39 '>50 frames per second', P:49 minimap): Julia 1920x1080 + colour levels, Mandelbrot minimap 240x180 + colour levels, C on the a=3.9 cardioid, max_iter 100, each tick synchronised; display excluded",
            "results": res}, open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/tick.json", "w"), indent=1)
