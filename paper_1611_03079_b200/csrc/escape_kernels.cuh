@@ -15,8 +15,8 @@
 //                             the escape test (block-end test + exact replay)
 //   escape_pathx_kernel   SX  C-path frames, FP32_FAST: two x-adjacent pixels per lane
 //                             (packed FFMA2 loop), whole-sector count stores
-//   escape_cont2s_kernel  P2S experimental packed P2 (two orbits per lane), with the
-//   escape_replay_kernel  P3  replay kernel for its exact escape indices (off by default)
+//   escape_cont2s_kernel  P2S experimental packed P2 (two orbits per lane, stashes, batched
+//                             in-warp replay; off by default)
 //   colorize_kernel           count -> RGBA colour levels (HBM-bound)
 // All iteration goes through Iter<T, STRICT>::step / core or the PTX vote loops, which
 // implement the same operation sequences (FAST: doubled state, FMA-contracted; STRICT:
@@ -1486,83 +1486,129 @@ __device__ __forceinline__ float2 fneg2(float2 a) { return make_float2(-a.x, -a.
 // kept and one |Z|^2 test per slot at the block end.  On cfg3's survivors the 64 slots
 // of a warp finish ~8 times per 32-iteration block, so finishing must be cheap and
 // mostly non-collective:
-//   * a finished slot writes its replay record (the start of its escaping sub-block and
-//     its index; "nothing to replay" for the iteration limit) over its consumed queue
-//     item, and continues with its stash, an item already in registers;
-//   * the emptied stashes are refilled by plain per-lane loads at ranked positions of a
-//     warp-private range of queue positions (reserved 128 at a time by one atomic, the
-//     next range reserved ahead), so the load latency is hidden by the orbit it stands
-//     behind (hundreds of iterations) -- no shared memory, no shuffles.
-// P3 (escape_replay_kernel) recovers the exact escape indices afterwards.
+//   * a finished slot that escaped appends a replay record (the start of its escaping
+//     sub-block and its index) to a per-warp buffer in shared memory; an interior one
+//     stores max_iter directly;
+//   * it continues with its stash, an item already in registers; emptied stashes are
+//     refilled by plain per-lane loads at ranked positions of a warp-private range of
+//     queue positions (RG per atomic, the next range reserved ahead), so the load
+//     latency hides behind the orbit in front of it -- no shuffles;
+//   * once 64 records are pending the warp replays them together, two per lane in the
+//     packed loop with the per-iteration test (<= KS steps, vote exit), and stores the
+//     exact counts: SIMT-efficient and without a global round trip.
 // ----------------------------------------------------------------------------------
 template <bool MANDEL, bool COLOR, int K>
 __global__ void __launch_bounds__(kThreads)
 escape_cont2s_kernel(const Geom g, const PalRef pal, const float jcr2, const float jci2,
-                     ContQueue* q, QItem<float>* items) {
+                     ContQueue* q, const QItem<float>* items) {
   constexpr int KS = 8, NS = K / KS;
   static_assert(K % KS == 0 && NS >= 1 && NS <= 8, "blocks of sub-blocks of 8");
-  constexpr unsigned RG = 128;  // queue positions per range reservation
+  constexpr unsigned RG = 32;   // queue positions per range reservation
+  constexpr unsigned PB = 128;  // pending replay records per warp (ring; <= 127 live)
+  __shared__ QItem<float> pend_buf[kThreads / 32][PB];
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const int max_iter = g.max_iter;
   const unsigned n_items = *reinterpret_cast<volatile unsigned*>(&q->tail);
   unsigned long long* trace = g_refill_trace;
-  const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + warp;
   if (trace && lane == 0) trace[gw * 3] = global_ns();
+  QItem<float>* pb = pend_buf[warp];
+  unsigned ph = 0u, pn = 0u;  // pending ring: head, count (warp-uniform)
   auto c_of = [&](unsigned idx, float& cr, float& ci) {
     const int row = (int)(idx / (unsigned)g.W);
     const int px = (int)(idx - (unsigned)row * (unsigned)g.W);
     cr = to_state<float, false>(pixel_re(g, px));
     ci = to_state<float, false>(pixel_im(g, global_row(g, row)));
   };
+  const float2 HALF = make_float2(0.5f, 0.5f);
+  // replay up to 64 pending records (two per lane, packed) and store their counts
+  auto replay = [&](unsigned n) {
+    const unsigned s0 = (ph + (unsigned)lane) & (PB - 1), s1 = (ph + 32u + (unsigned)lane) & (PB - 1);
+    const bool a = (unsigned)lane < n, b = (unsigned)lane + 32u < n;
+    QItem<float> r0{}, r1{};
+    if (a) r0 = pb[s0];
+    if (b) r1 = pb[s1];
+    float2 x = make_float2(r0.x, r1.x), y = make_float2(r0.y, r1.y);
+    float2 cr = make_float2(jcr2, jcr2), ci = make_float2(jci2, jci2);
+    if (MANDEL) {
+      if (a) c_of(r0.idx, cr.x, ci.x);
+      if (b) c_of(r1.idx, cr.y, ci.y);
+    }
+    bool pa = a, pb_ = b;
+    int na = 0, nb = 0;
+#pragma unroll 1
+    for (int j = 0; j < KS; ++j) {
+      if (!__any_sync(kFull, pa || pb_)) break;
+      const float2 m = ffma2(x, x, fmul2(y, y));
+      pa = pa && (m.x <= 16.0f);
+      pb_ = pb_ && (m.y <= 16.0f);
+      if (pa) ++na;
+      if (pb_) ++nb;
+      const float2 YY = fmul2(y, y);
+      const float2 T = ffma2(x, x, fneg2(YY));
+      const float2 Yn = ffma2(x, y, ci);
+      x = ffma2(T, HALF, cr);
+      y = Yn;
+    }
+    // na == KS: the sub-block's end state escaped
+    if (a) {
+      const int c0 = r0.cnt + na;
+      const int count = c0 < max_iter ? c0 : max_iter;
+      g.counts[r0.idx] = (uint16_t)count;
+      if (COLOR) g.rgba[r0.idx] = colour_dev(pal, count, max_iter);
+    }
+    if (b) {
+      const int c0 = r1.cnt + nb;
+      const int count = c0 < max_iter ? c0 : max_iter;
+      g.counts[r1.idx] = (uint16_t)count;
+      if (COLOR) g.rgba[r1.idx] = colour_dev(pal, count, max_iter);
+    }
+    __syncwarp();
+    ph = (ph + n) & (PB - 1);
+    pn -= n;
+  };
   // ---- warp-private queue ranges: current [r0, r1), next [nx, nx + RG) (reserved)
   unsigned r0 = 0u, r1 = 0u, nx = 0u;
   bool exhausted = false;
   {
     unsigned b = 0u;
-    if (lane == 0) b = atomicAdd(&q->head, RG);
+    if (lane == 0) b = atomicAdd(&q->head, 4u * 32u);  // slots + stashes
     r0 = __shfl_sync(kFull, b, 0);
-    r1 = r0 + RG;
     if (lane == 0) nx = atomicAdd(&q->head, RG);  // lane 0 only, until shuffled
   }
-  // slots and stashes: the first 128 positions of the range, in that order
   float2 X, Y;
   float2 CR = make_float2(jcr2, jcr2), CI = make_float2(jci2, jci2);
   int ca, cb;
-  unsigned ia, ib, qa, qb;
+  unsigned ia, ib;
   bool ha, hb;
   QItem<float> sa{}, sb{};
-  unsigned sqa = 0u, sqb = 0u;
   bool va, vb;
   {
-    const unsigned pa = r0 + (unsigned)lane, pb = pa + 32u, psa = pa + 64u, psb = pa + 96u;
+    const unsigned pa = r0 + (unsigned)lane, pb2 = pa + 32u, psa = pa + 64u, psb = pa + 96u;
     QItem<float> ta{}, tb{};
     ha = pa < n_items;
-    hb = pb < n_items;
+    hb = pb2 < n_items;
     va = psa < n_items;
     vb = psb < n_items;
     if (ha) ta = items[pa];
-    if (hb) tb = items[pb];
+    if (hb) tb = items[pb2];
     if (va) sa = items[psa];
     if (vb) sb = items[psb];
-    sqa = psa;
-    sqb = psb;
     X = make_float2(ta.x, tb.x);
     Y = make_float2(ta.y, tb.y);
     ca = ta.cnt;
     cb = tb.cnt;
     ia = ta.idx;
     ib = tb.idx;
-    qa = pa;
-    qb = pb;
     if (MANDEL) {
       if (ha) c_of(ia, CR.x, CI.x);
       if (hb) c_of(ib, CR.y, CI.y);
     }
-    r0 = r1;  // the first range is used up
-    exhausted = r0 >= n_items && __shfl_sync(kFull, nx, 0) >= n_items;
+    r0 = r1 = 0u;  // the first block of positions is used up
+    exhausted = __shfl_sync(kFull, nx, 0) >= n_items;
   }
-  const float2 HALF = make_float2(0.5f, 0.5f);
   for (;;) {
     if (!__any_sync(kFull, ha || hb)) break;
     float2 CX[NS], CY[NS];
@@ -1586,7 +1632,7 @@ escape_cont2s_kernel(const Geom g, const PalRef pal, const float jcr2, const flo
     if (ha && !fa) ca += K;
     if (hb && !fb) cb += K;
     if (!__any_sync(kFull, fa || fb)) continue;
-    // ---- finished slots: replay record (or the interior count) over the consumed item
+    // ---- finished slots: pending replay record (escaped) or the interior count
     {
       float2 sx = CX[NS - 1], sy = CY[NS - 1];
       int oa = (NS - 1) * KS, ob = (NS - 1) * KS;
@@ -1596,33 +1642,44 @@ escape_cont2s_kernel(const Geom g, const PalRef pal, const float jcr2, const flo
         if (!(m.x <= 16.0f)) { sx.x = CX[s2].x; sy.x = CY[s2].x; oa = s2 * KS; }
         if (!(m.y <= 16.0f)) { sx.y = CX[s2].y; sy.y = CY[s2].y; ob = s2 * KS; }
       }
-      if (fa) {
+      const bool ra = fa && ea, rb = fb && eb;
+      const unsigned qa_m = __ballot_sync(kFull, ra), qb_m = __ballot_sync(kFull, rb);
+      const unsigned ka = (unsigned)__popc(qa_m & lt);
+      const unsigned kb = (unsigned)__popc(qa_m) + (unsigned)__popc(qb_m & lt);
+      if (ra) {
         QItem<float> r;
-        r.x = sx.x; r.y = sy.x; r.cnt = ea ? ca + oa : -1; r.idx = ia;
-        items[qa] = r;
-        if (!ea) {
-          g.counts[ia] = (uint16_t)max_iter;
-          if (COLOR) g.rgba[ia] = pal.interior;
-        }
-        // continue with the stash
-        X.x = sa.x; Y.x = sa.y; ca = sa.cnt; ia = sa.idx; qa = sqa;
+        r.x = sx.x; r.y = sy.x; r.cnt = ca + oa; r.idx = ia;
+        pb[(ph + pn + ka) & (PB - 1)] = r;
+      }
+      if (rb) {
+        QItem<float> r;
+        r.x = sx.y; r.y = sy.y; r.cnt = cb + ob; r.idx = ib;
+        pb[(ph + pn + kb) & (PB - 1)] = r;
+      }
+      pn += (unsigned)(__popc(qa_m) + __popc(qb_m));
+      if (fa && !ea) {
+        g.counts[ia] = (uint16_t)max_iter;
+        if (COLOR) g.rgba[ia] = pal.interior;
+      }
+      if (fb && !eb) {
+        g.counts[ib] = (uint16_t)max_iter;
+        if (COLOR) g.rgba[ib] = pal.interior;
+      }
+      // continue with the stash
+      if (fa) {
+        X.x = sa.x; Y.x = sa.y; ca = sa.cnt; ia = sa.idx;
         ha = va;
         va = false;
         if (MANDEL && ha) c_of(ia, CR.x, CI.x);
       }
       if (fb) {
-        QItem<float> r;
-        r.x = sx.y; r.y = sy.y; r.cnt = eb ? cb + ob : -1; r.idx = ib;
-        items[qb] = r;
-        if (!eb) {
-          g.counts[ib] = (uint16_t)max_iter;
-          if (COLOR) g.rgba[ib] = pal.interior;
-        }
-        X.y = sb.x; Y.y = sb.y; cb = sb.cnt; ib = sb.idx; qb = sqb;
+        X.y = sb.x; Y.y = sb.y; cb = sb.cnt; ib = sb.idx;
         hb = vb;
         vb = false;
         if (MANDEL && hb) c_of(ib, CR.y, CI.y);
       }
+      __syncwarp();
+      if (pn >= 64u) replay(64u);
     }
     if (exhausted) continue;
     // ---- refill the emptied stashes from the warp's ranges (per-lane loads)
@@ -1630,24 +1687,38 @@ escape_cont2s_kernel(const Geom g, const PalRef pal, const float jcr2, const flo
     const unsigned m = (unsigned)(__popc(ma) + __popc(mb));
     const unsigned ka = (unsigned)__popc(ma & lt);
     const unsigned kb = (unsigned)__popc(ma) + (unsigned)__popc(mb & lt);
-    const unsigned cur = r1 - r0;  // positions left in the current range
-    const unsigned nb = __shfl_sync(kFull, nx, 0);
-    auto pos_of = [&](unsigned k) { return k < cur ? r0 + k : nb + (k - cur); };
+    unsigned cur = r1 - r0;
+    unsigned nb = __shfl_sync(kFull, nx, 0);
+    // (m <= 64 may need up to two fresh ranges beyond the current one)
+    unsigned nb2 = 0u;
+    if (m > cur + RG) {
+      if (lane == 0) nb2 = atomicAdd(&q->head, RG);
+      nb2 = __shfl_sync(kFull, nb2, 0);
+    }
+    auto pos_of = [&](unsigned k) {
+      return k < cur ? r0 + k : (k < cur + RG ? nb + (k - cur) : nb2 + (k - cur - RG));
+    };
     if (fa) {
-      sqa = pos_of(ka);
-      va = sqa < n_items;
-      if (va) sa = items[sqa];
+      const unsigned p = pos_of(ka);
+      va = p < n_items;
+      if (va) sa = items[p];
     }
     if (fb) {
-      sqb = pos_of(kb);
-      vb = sqb < n_items;
-      if (vb) sb = items[sqb];
+      const unsigned p = pos_of(kb);
+      vb = p < n_items;
+      if (vb) sb = items[p];
     }
     if (m < cur) {
       r0 += m;
-    } else {  // moved into the next range: reserve the one after it
-      r0 = nb + (m - cur);
-      r1 = nb + RG;
+    } else {  // moved into the next range(s): reserve the one after
+      if (m < cur + RG) {
+        r0 = nb + (m - cur);
+        r1 = nb + RG;
+      } else {
+        r0 = nb2 + (m - cur - RG);
+        r1 = nb2 + RG;
+        nb = nb2;
+      }
       if (lane == 0) nx = atomicAdd(&q->head, RG);
       if (nb >= n_items) {
         exhausted = true;
@@ -1655,46 +1726,13 @@ escape_cont2s_kernel(const Geom g, const PalRef pal, const float jcr2, const flo
       }
     }
   }
+  while (pn > 0u) replay(pn < 64u ? pn : 64u);
   if (trace && lane == 0) trace[gw * 3 + 2] = global_ns();
-}
-
-// P3: exact escape index of P2S's replay records, one record per thread: the FAST step
-// with the per-iteration test from the recorded block-start state Z_cnt (the record's
-// block escaped at its end state, so the loop ends within K steps).  Resets the queue
-// header when the last CTA finishes (the next call's P1 appends from 0).
-template <bool MANDEL, bool COLOR, int K>
-__global__ void __launch_bounds__(kThreads)
-escape_replay_kernel(const Geom g, const PalRef pal, const float jcr2, const float jci2,
-                     ContQueue* q, const QItem<float>* items) {
-  const unsigned n_items = *reinterpret_cast<volatile unsigned*>(&q->tail) +
-                           *reinterpret_cast<volatile unsigned*>(&q->left);
-  const unsigned stride = gridDim.x * kThreads;
-  for (unsigned i = blockIdx.x * kThreads + threadIdx.x; i < n_items; i += stride) {
-    const QItem<float> r = items[i];
-    if (r.cnt < 0) continue;
-    float x = r.x, y = r.y, cr = jcr2, ci = jci2;
-    if (MANDEL) {
-      const int row = (int)(r.idx / (unsigned)g.W);
-      const int px = (int)(r.idx - (unsigned)row * (unsigned)g.W);
-      cr = to_state<float, false>(pixel_re(g, px));
-      ci = to_state<float, false>(pixel_im(g, global_row(g, row)));
-    }
-    int j = 0;
-    for (; j < K; ++j) {
-      if (!(Iter<float, false>::mag(x, y) <= 16.0f)) break;
-      Iter<float, false>::core(x, y, cr, ci);
-    }
-    const int c0 = r.cnt + j;  // j == K: the block's end state (it escaped)
-    const int count = c0 < g.max_iter ? c0 : g.max_iter;
-    g.counts[r.idx] = (uint16_t)count;
-    if (COLOR) g.rgba[r.idx] = colour_dev(pal, count, g.max_iter);
-  }
-  // ---- self-reset of the queue by the last CTA
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  // ---- self-reset of the queue by the last warp to finish
+  if (lane == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(&q->done_warps, 1u);
-    if (prev == gridDim.x - 1) {
+    if (prev == gridDim.x * (kThreads / 32) - 1) {
       q->tail = 0u;
       q->head = 0u;
       q->left = 0u;

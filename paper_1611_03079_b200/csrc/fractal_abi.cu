@@ -532,7 +532,7 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  // FP32_FAST under the precondition: the packed two-slot P2 with stashes (P2S) + P3
+  // FP32_FAST under the precondition: the packed two-slot P2 with stashes (P2S)
   // (FRACTAL_P2S=0 falls back; FRACTAL_P2S_K: block 16/32/64)
   if constexpr (!STRICT && std::is_same<T, float>::value) {
     if (amort && p2s_on()) {
@@ -540,7 +540,6 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
       auto k2 = fr::escape_cont2s_kernel<MANDEL, COLOR, 32>;
       if (ks == 16) k2 = fr::escape_cont2s_kernel<MANDEL, COLOR, 16>;
       else if (ks == 64) k2 = fr::escape_cont2s_kernel<MANDEL, COLOR, 64>;
-      auto k3 = fr::escape_replay_kernel<MANDEL, COLOR, 8>;
       static const int occs = [&] {
         int o = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k2, fr::kThreads, 0) !=
@@ -554,12 +553,6 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
       k2<<<(unsigned)(sm_count() * o2), fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, q,
                                                               items);
       e = cudaGetLastError();
-      if (e == cudaSuccess) {
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        k3<<<(unsigned)(sm_count() * 8), fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, q,
-                                                               items);
-        e = cudaGetLastError();
-      }
       if (e != cudaSuccess) {
         cudaMemsetAsync(qp, 0, sizeof(fr::ContQueue), s);
         return e;

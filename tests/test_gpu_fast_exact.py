@@ -178,3 +178,66 @@ def test_fast_nonmonotone_mandelbrot_window(fr, prec):
     for mi in (100, 1000):
         ref = oracle.mandelbrot(win.center, win.half_w, win.half_h, 301, 183, mi, prec, fast=True)
         np.testing.assert_array_equal(gpu_mandel(fr, win, 301, 183, mi, fast(prec, fr)), ref)
+
+
+@pytest.mark.parametrize("w,h", [(37, 5), (48, 9), (65, 17), (130, 7), (1, 1)])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_fast_path_kernel_sx_layouts(fr, w, h, offset):
+    """Kernel SX (FP32_FAST C-paths: x-adjacent pixel pairs, 4-byte count stores and
+    8-byte RGBA stores when the pair is whole and aligned): odd widths, an output pointer
+    one element off alignment (scalar stores), uint16 and uint8 counts, fused colour --
+    every frame equal to the FAST oracle, nothing written outside the buffers."""
+    cs = W.circle_path(37)
+    win = W.julia_window(w, h)
+    pal = W.palette("fire")
+    n = len(cs)
+    g = 64
+    base16 = torch.full((n * h * w + 2 * g + offset,), -1, dtype=torch.int16, device="cuda")
+    out16 = base16[g + offset:g + offset + n * h * w].view(torch.uint16).view(n, h, w)
+    base8 = torch.full((n * h * w + 2 * g + offset,), 0xAB, dtype=torch.uint8, device="cuda")
+    out8 = base8[g + offset:g + offset + n * h * w].view(n, h, w)
+    baser = torch.full((4 * (n * h * w + 2 * g + offset),), 0x5A, dtype=torch.uint8,
+                       device="cuda")
+    rgba = baser[4 * (g + offset):4 * (g + offset + n * h * w)].view(n, h, w, 4)
+    fr.julia_render_path(cs, win, w, h, 100, fr.Mode.FP32_FAST, out=out16, palette=pal,
+                         out_rgba=rgba)
+    fr.julia_render_path(cs, win, w, h, 100, fr.Mode.FP32_FAST, out=out8)
+    torch.cuda.synchronize()
+    a16 = base16.cpu().numpy()
+    assert (a16[:g + offset] == -1).all() and (a16[g + offset + n * h * w:] == -1).all()
+    a8 = base8.cpu().numpy()
+    assert (a8[:g + offset] == 0xAB).all() and (a8[g + offset + n * h * w:] == 0xAB).all()
+    ar = baser.cpu().numpy()
+    assert (ar[:4 * (g + offset)] == 0x5A).all() and (ar[4 * (g + offset + n * h * w):] == 0x5A).all()
+    got16, got8, gotr = np16(out16), out8.cpu().numpy(), rgba.cpu().numpy()
+    for k in range(n):
+        ref = oracle.julia(complex(cs[k]), win.center, win.half_w, win.half_h, w, h, 100, 32,
+                           fast=True)
+        np.testing.assert_array_equal(got16[k], ref)
+        np.testing.assert_array_equal(got8[k], ref.astype(np.uint8))
+        np.testing.assert_array_equal(gotr[k], oracle.colorize(ref, 100, *pal))
+
+
+def test_fast_cfg4_all_frames(fr):
+    """cfg4 in FP32_FAST at full size, ALL 4096 frames (kernel SX, the bench kernel)
+    against the FAST oracle, frame by frame."""
+    from concurrent.futures import ThreadPoolExecutor
+    cfg = W.configs()["cfg4"]
+    cs = W.circle_path(cfg.n_frames)
+    win = cfg.window
+    out = fr.julia_render_path(cs, win, cfg.width, cfg.height, cfg.max_iter, fr.Mode.FP32_FAST)
+    torch.cuda.synchronize()
+
+    def ref(k):
+        return oracle.julia(complex(cs[k]), win.center, win.half_w, win.half_h, cfg.width,
+                            cfg.height, cfg.max_iter, 32, threads=2, fast=True)
+
+    bad = []
+    with ThreadPoolExecutor(max(1, oracle.default_threads() // 2)) as ex:
+        for k0 in range(0, cfg.n_frames, 64):
+            refs = list(ex.map(ref, range(k0, min(k0 + 64, cfg.n_frames))))
+            got = out[k0:k0 + len(refs)].view(torch.int16).cpu().numpy().view(np.uint16)
+            bad += [k0 + i for i, r in enumerate(refs) if not np.array_equal(got[i], r)]
+    assert not bad, f"{len(bad)} frames differ, first {bad[:8]}"
+    del out
+    torch.cuda.empty_cache()
