@@ -37,5 +37,27 @@ for n in (10, 100, 316, 1000):
         row[name] = {"one_call_us_median": float(np.median(ts)),
                      "back_to_back_us": a.elapsed_time(b) * 1e3 / 2000,
                      "host_submit_us": host_us}
+    # the plan's call captured once into a CUDA graph (fixed C), replayed back to back
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        gplan = fr.FramePlan("julia", (0j, 1.5, 1.5), n, n, 100, fr.Mode.FP32_FAST, out=out,
+                             stream=s)
+        gplan.render(C)  # eager first call on the stream (workspaces, outside capture)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            gplan.render(C)
+    torch.cuda.synchronize()
+    for _ in range(20):
+        g.replay()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(2000):
+        g.replay()
+    b.record()
+    b.synchronize()
+    row["plan_graph_replay"] = {"back_to_back_us": a.elapsed_time(b) * 1e3 / 2000}
     res[n] = row
     print(json.dumps({"side": n, **row}), flush=True)
