@@ -263,6 +263,22 @@ struct Iter<double, false> {
   }
 };
 
+// Packed-float helpers (sm_100 FFMA2 / FMUL2: two separately rounded operations).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fneg2(float2 a) { return make_float2(-a.x, -a.y); }
+// One FAST step on both halves (the doubled FMA sequence of Iter<float, false>::core).
+__device__ __forceinline__ void fast_core2(float2& X, float2& Y, const float2 CR, const float2 CI) {
+  const float2 YY = fmul2(Y, Y);
+  const float2 T = ffma2(X, X, fneg2(YY));
+  const float2 Yn = ffma2(X, Y, CI);
+  X = ffma2(T, make_float2(0.5f, 0.5f), CR);
+  Y = Yn;
+}
+__device__ __forceinline__ float2 fast_mag2(const float2 X, const float2 Y) {
+  return ffma2(X, X, fmul2(Y, Y));
+}
+
 // NEXT-3 iteration maps (Figure 4, reading c-14), strict op sequence in
 // both modes, identical to the oracle's: w = z^2 = (xx - yy, xy + xy); z^4 = w^2;
 // rational term q = (w + 1)/(w - 1) = ((a c + b d) + i (b c - a d))/(c^2 + d^2) with
@@ -1000,13 +1016,15 @@ escape_tile2_kernel(const Geom g, const PalRef pal, const float jcr2, const floa
   unsigned alive = in0 ? 1u : 0u, alive2 = in1 ? 1u : 0u;
   int cnt = 0, cnt2 = 0;
   const int max_iter = g.max_iter;
-  const int kfull = max_iter - max_iter % KV;
-  int n = vote_loop2_f32<STRICT, KV>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2,
-                                     kfull);
-  if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
-    for (; n < max_iter; ++n) {
-      Iter<float, STRICT>::step(x, y, cr, ci, alive, cnt);
-      Iter<float, STRICT>::step(x2, y2, cr2, ci2, alive2, cnt2);
+  {
+    const int kfull = max_iter - max_iter % KV;
+    int n = vote_loop2_f32<STRICT, KV>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2,
+                                       ci2, kfull);
+    if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
+      for (; n < max_iter; ++n) {
+        Iter<float, STRICT>::step(x, y, cr, ci, alive, cnt);
+        Iter<float, STRICT>::step(x2, y2, cr2, ci2, alive2, cnt2);
+      }
     }
   }
   if (in0) {
@@ -1118,8 +1136,8 @@ __device__ __forceinline__ void budget_tile(const Geom& g, const PalRef& pal, co
     int n0 = 0;
     if constexpr (PRE > 0) {
       if constexpr (kAsmPair<T, STRICT, 4>) {
-        n0 = vote_loop2_f32<STRICT>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2,
-                                    PRE);
+        n0 = vote_loop2_f32<STRICT, KV>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2,
+                                        ci2, PRE);
       } else {
         for (; n0 < PRE; n0 += 4) {
 #pragma unroll
@@ -1136,8 +1154,55 @@ __device__ __forceinline__ void budget_tile(const Geom& g, const PalRef& pal, co
     // d: the end state of some sub-block escaped (sticky; NaN/inf count as escaped);
     // (xc, yc) = start state of the first such sub-block, cnt = its first index
     bool d0 = !p0, d1 = !p1;
-    T xc = x, yc = y, xc2 = x2, yc2 = y2;
     if (!__any_sync(kFull, p0 || p1)) n0 = budget;
+    if constexpr (std::is_same<T, float>::value) {
+      // binary32: both orbits in packed registers (FFMA2/FMUL2)
+      float2 X = make_float2(x, x2), Y = make_float2(y, y2);
+      const float2 CRp = make_float2(cr, cr2), CIp = make_float2(ci, ci2);
+      float2 XC = X, YC = Y;
+      for (int n = n0; n < budget; n += KS) {
+        if (!d0) {
+          XC.x = X.x;
+          YC.x = Y.x;
+          cnt = n;
+        }
+        if (!d1) {
+          XC.y = X.y;
+          YC.y = Y.y;
+          cnt2 = n;
+        }
+#pragma unroll
+        for (int j = 0; j < KS; ++j) fast_core2(X, Y, CRp, CIp);
+        const float2 M = fast_mag2(X, Y);
+        d0 = d0 || !(M.x <= 16.0f);
+        d1 = d1 || !(M.y <= 16.0f);
+        if (__all_sync(kFull, d0 && d1)) break;
+      }
+      if (!d0) cnt = budget;
+      if (!d1) cnt2 = budget;
+      alive = !d0 ? 1u : 0u;
+      alive2 = !d1 ? 1u : 0u;
+      const bool q0 = p0 && d0, q1 = p1 && d1;
+      bool ra = q0, rb = q1;
+      int rc = 0, rc2 = 0;
+#pragma unroll 1
+      for (int j = 0; j < KS; ++j) {
+        if (!__any_sync(kFull, ra || rb)) break;
+        const float2 m = fast_mag2(XC, YC);
+        ra = ra && (m.x <= 16.0f);
+        rb = rb && (m.y <= 16.0f);
+        if (ra) ++rc;
+        if (rb) ++rc2;
+        fast_core2(XC, YC, CRp, CIp);
+      }
+      if (q0) cnt += rc;
+      if (q1) cnt2 += rc2;
+      x = X.x;
+      y = Y.x;
+      x2 = X.y;
+      y2 = Y.y;
+    } else {
+    T xc = x, yc = y, xc2 = x2, yc2 = y2;
     for (int n = n0; n < budget; n += KS) {
       if (!d0) {
         xc = x;
@@ -1180,6 +1245,7 @@ __device__ __forceinline__ void budget_tile(const Geom& g, const PalRef& pal, co
     }
     if (q0) cnt += rc;
     if (q1) cnt2 += rc2;
+    }
   } else if constexpr (kAsmPair<T, STRICT, 4>) {
     vote_loop2_f32<STRICT, KV>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr2, ci2,
                                budget);
@@ -1474,10 +1540,6 @@ escape_cont_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Co
   }
 }
 
-// Packed-float helpers (sm_100 FFMA2 / FMUL2: two separately rounded operations).
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-__device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
-__device__ __forceinline__ float2 fneg2(float2 a) { return make_float2(-a.x, -a.y); }
 
 // ----------------------------------------------------------------------------------
 // "P2S" (experimental, FRACTAL_P2S=1): P2 for FP32_FAST under the

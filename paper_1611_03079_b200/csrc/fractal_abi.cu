@@ -446,9 +446,12 @@ constexpr int64_t kTwoPhaseMaxPixels = int64_t(1) << 25;  // item buffer <= 1 Gi
 // 0.1679/0.1685/0.1719 ms)
 // fp64 fast with the amortised P1 (below): 64 (cfg3 FP64_FAST, KS 8, prefix 8: budget
 // 32/40/48/64 0.2459/0.2442/0.2443/0.2433 ms; exact P1 at 48 0.2464)
+// fp32 fast with the packed amortised P1 (round 2): 128 (cfg3, KS 8, prefix 8 / 16:
+// budget 96/128/160/192/256 0.1647/0.1630-0.1637/0.1652/0.1670/0.1735 ms against the
+// exact P1 at 48 0.1655; profiles/r02/ab_p1_packed_amort.txt)
 int twophase_budget(bool amort, bool f64) {
   static const int b = env_int("FRACTAL_BUDGET", 0);
-  const int v = b > 0 ? b : (amort ? (f64 ? 64 : 48) : 96);
+  const int v = b > 0 ? b : (amort ? (f64 ? 64 : 128) : 96);
   return v < 4 ? 4 : v - v % 4;
 }
 
@@ -458,11 +461,11 @@ bool p2s_on() {  // experimental packed P2: off, slower than the
 }
 
 
-#ifndef FR_P1A_KS  // amortised P1 sub-block (0 = exact per-iteration test)
-#define FR_P1A_KS 0
+#ifndef FR_P1A_KS  // amortised P1 sub-block in fp32 (0 = exact per-iteration test)
+#define FR_P1A_KS 8
 #endif
 #ifndef FR_P1A_PRE
-#define FR_P1A_PRE 0
+#define FR_P1A_PRE 8
 #endif
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH, int KA, int THA>
 cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double2 c,
