@@ -1542,131 +1542,6 @@ escape_cont_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Co
 
 
 // ----------------------------------------------------------------------------------
-// "PC": one compaction phase for FP32_FAST under the escape-monotonicity precondition.
-// P1 leaves the survivors of its budget in a dense queue; a phase takes them 64 at a
-// time per warp (two per lane, packed), runs the packed amortised sub-blocks of the
-// budgeted P1 (one |Z|^2 test per orbit per KS iterations, start state of the escaping
-// sub-block kept, one deferred replay) up to the iteration n_end, stores the counts
-// (and colours) of the orbits that escaped, and appends the survivors -- state Z_n_end
-// -- densely to the next queue.  Orbits of a warp start together and, after P1, have
-// similar remaining lengths within a budget window, so a static warp of 64 wastes
-// little (cfg3: 0.77 of the lane-iterations useful in windows of 128, oracle-count
-// model), and the loop is FMA-pipe-bound with no per-iteration ALU work.  A chain of
-// phases (128 iterations each) precedes the lane-refill P2, which then only sees the
-// long tail.  The last warp to finish resets the input queue header.
-// ----------------------------------------------------------------------------------
-template <bool MANDEL, bool COLOR, int KS>
-__global__ void __launch_bounds__(kThreads)
-escape_phase_kernel(const Geom g, const PalRef pal, const float jcr2, const float jci2,
-                    int n_end, ContQueue* qin, const QItem<float>* in, ContQueue* qout,
-                    QItem<float>* out) {
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
-  const int max_iter = g.max_iter;
-  const unsigned n_items = *reinterpret_cast<volatile unsigned*>(&qin->tail);
-  auto c_of = [&](unsigned idx, float& cr, float& ci) {
-    const int row = (int)(idx / (unsigned)g.W);
-    const int px = (int)(idx - (unsigned)row * (unsigned)g.W);
-    cr = to_state<float, false>(pixel_re(g, px));
-    ci = to_state<float, false>(pixel_im(g, global_row(g, row)));
-  };
-  for (;;) {
-    unsigned grp = 0u;
-    if (lane == 0) grp = atomicAdd(&qin->head, 64u);
-    grp = __shfl_sync(kFull, grp, 0);
-    if (grp >= n_items) break;
-    const unsigned ia_ = grp + (unsigned)lane, ib_ = ia_ + 32u;
-    const bool ha = ia_ < n_items, hb = ib_ < n_items;
-    QItem<float> ta{}, tb{};
-    if (ha) ta = in[ia_];
-    if (hb) tb = in[ib_];
-    float2 X = make_float2(ta.x, tb.x), Y = make_float2(ta.y, tb.y);
-    float2 CRp = make_float2(jcr2, jcr2), CIp = make_float2(jci2, jci2);
-    if (MANDEL) {
-      if (ha) c_of(ta.idx, CRp.x, CIp.x);
-      if (hb) c_of(tb.idx, CRp.y, CIp.y);
-    }
-    // all items of a queue start at the same iteration (the previous window's end)
-    const int n0 = __shfl_sync(kFull, ha ? ta.cnt : 0x7fffffff, 0);
-    bool d0 = !ha, d1 = !hb;
-    float2 XC = X, YC = Y;
-    int ca = n0, cb = n0;
-    int n = n0;
-    for (; n < n_end; n += KS) {
-      if (!d0) {
-        XC.x = X.x;
-        YC.x = Y.x;
-        ca = n;
-      }
-      if (!d1) {
-        XC.y = X.y;
-        YC.y = Y.y;
-        cb = n;
-      }
-#pragma unroll
-      for (int j = 0; j < KS; ++j) fast_core2(X, Y, CRp, CIp);
-      const float2 M = fast_mag2(X, Y);
-      d0 = d0 || !(M.x <= 16.0f);  // unordered: NaN/inf escaped
-      d1 = d1 || !(M.y <= 16.0f);
-      if (__all_sync(kFull, d0 && d1)) break;
-    }
-    // escaped: exact index by replaying the escaping sub-block
-    const bool qa = ha && d0, qb = hb && d1;
-    bool ra = qa, rb = qb;
-    int rc = 0, rc2 = 0;
-#pragma unroll 1
-    for (int j = 0; j < KS; ++j) {
-      if (!__any_sync(kFull, ra || rb)) break;
-      const float2 m = fast_mag2(XC, YC);
-      ra = ra && (m.x <= 16.0f);
-      rb = rb && (m.y <= 16.0f);
-      if (ra) ++rc;
-      if (rb) ++rc2;
-      fast_core2(XC, YC, CRp, CIp);
-    }
-    // not escaped by n_end: a survivor, or interior once n_end reaches max_iter
-    const bool sa = ha && !d0 && n_end < max_iter, sb = hb && !d1 && n_end < max_iter;
-    if (ha && !sa) {
-      const int count = qa ? min(ca + rc, max_iter) : max_iter;
-      g.counts[ta.idx] = (uint16_t)count;
-      if (COLOR) g.rgba[ta.idx] = colour_dev(pal, count, max_iter);
-    }
-    if (hb && !sb) {
-      const int count = qb ? min(cb + rc2, max_iter) : max_iter;
-      g.counts[tb.idx] = (uint16_t)count;
-      if (COLOR) g.rgba[tb.idx] = colour_dev(pal, count, max_iter);
-    }
-    const unsigned b0 = __ballot_sync(kFull, sa), b1 = __ballot_sync(kFull, sb);
-    if (b0 | b1) {
-      unsigned base = 0u;
-      if (lane == 0) base = atomicAdd(&qout->tail, (unsigned)(__popc(b0) + __popc(b1)));
-      base = __shfl_sync(kFull, base, 0);
-      if (sa) {
-        QItem<float> it;
-        it.x = X.x; it.y = Y.x; it.cnt = n_end; it.idx = ta.idx;
-        out[base + (unsigned)__popc(b0 & lt)] = it;
-      }
-      if (sb) {
-        QItem<float> it;
-        it.x = X.y; it.y = Y.y; it.cnt = n_end; it.idx = tb.idx;
-        out[base + (unsigned)__popc(b0) + (unsigned)__popc(b1 & lt)] = it;
-      }
-    }
-  }
-  // ---- the last warp resets the input queue (the next call's producer starts from 0)
-  if (lane == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(&qin->done_warps, 1u);
-    if (prev == gridDim.x * (kThreads / 32) - 1) {
-      qin->tail = 0u;
-      qin->head = 0u;
-      qin->done_warps = 0u;
-      __threadfence();
-    }
-  }
-}
-
-// ----------------------------------------------------------------------------------
 // "P2S" (experimental, FRACTAL_P2S=1): P2 for FP32_FAST under the
 // escape-monotonicity precondition with two orbits ("slots") per lane in packed float2
 // registers (FFMA2/FMUL2), blocks of K bare iterations with the sub-block start states

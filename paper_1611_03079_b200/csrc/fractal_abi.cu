@@ -438,7 +438,7 @@ cudaError_t launch_refill_t(const fr::Geom& g, const fr::Palette& pal, double2 c
 
 // Two-phase kernels P1 + P2: the queue header (zeroed once per (device, stream), reset by
 // P2's last warp) and an item buffer of one QItem per pixel of the call, grown on demand.
-std::map<std::pair<int, uintptr_t>, std::pair<void*, size_t>> g_queue, g_items, g_items2;
+std::map<std::pair<int, uintptr_t>, std::pair<void*, size_t>> g_queue, g_items;
 constexpr int64_t kTwoPhaseMaxPixels = int64_t(1) << 25;  // item buffer <= 1 GiB (fp64)
 
 // P1's budget (FRACTAL_BUDGET, multiple of 4): 96 before an exact P2, 48 before the
@@ -482,11 +482,10 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
     std::lock_guard<std::mutex> lock(g_ws_mutex);
     fresh = g_queue.find(std::make_pair(dev, (uintptr_t)s)) == g_queue.end();
   }
-  // two queue headers: P1's output and the ping-pong partner of the compaction phases
-  cudaError_t e = buffer_for(g_queue, s, 2 * sizeof(fr::ContQueue), &qp);
+  cudaError_t e = buffer_for(g_queue, s, sizeof(fr::ContQueue), &qp);
   if (e != cudaSuccess) return e;
   if (fresh) {  // zeroed in stream order on `s`, before P1 appends to it
-    e = cudaMemsetAsync(qp, 0, 2 * sizeof(fr::ContQueue), s);
+    e = cudaMemsetAsync(qp, 0, sizeof(fr::ContQueue), s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return e;
   }
@@ -558,53 +557,11 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
                                                               items);
       e = cudaGetLastError();
       if (e != cudaSuccess) {
-        cudaMemsetAsync(qp, 0, 2 * sizeof(fr::ContQueue), s);
+        cudaMemsetAsync(qp, 0, sizeof(fr::ContQueue), s);
         return e;
       }
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return cudaSuccess;
-    }
-  }
-  // FP32_FAST under the precondition: compaction phases (PC) of `phase_window()`
-  // iterations each between P1 and P2 (FRACTAL_PHASES: how many; 0 = none), ping-pong
-  // between the two queues; P2 then continues from the last one
-  fr::ContQueue* q2 = q;
-  fr::QItem<T>* items2 = items;
-  if constexpr (!STRICT && std::is_same<T, float>::value) {
-    static const int nph = env_int("FRACTAL_PHASES", 0);
-    static const int win = env_int("FRACTAL_PHASE_W", 128);
-    if (amort && nph > 0 && win % 8 == 0) {
-      void* ip2 = nullptr;
-      e = buffer_for(g_items2, s, (size_t)n * sizeof(fr::QItem<T>), &ip2);
-      if (e != cudaSuccess) return e;
-      auto kp = fr::escape_phase_kernel<MANDEL, COLOR, 8>;
-      static const int occp = [&] {
-        int o = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kp, fr::kThreads, 0) !=
-                cudaSuccess || o <= 0)
-          o = 1;
-        return o;
-      }();
-      fr::ContQueue* qa = q;
-      fr::QItem<T>* ia = items;
-      fr::ContQueue* qb = q + 1;
-      fr::QItem<T>* ib = static_cast<fr::QItem<T>*>(ip2);
-      int n_end = budget;
-      for (int ph = 0; ph < nph && n_end < g.max_iter; ++ph) {
-        n_end += win;
-        kp<<<(unsigned)(sm_count() * occp), fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci,
-                                                                  n_end, qa, ia, qb, ib);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) {
-          cudaMemsetAsync(qp, 0, 2 * sizeof(fr::ContQueue), s);
-          return e;
-        }
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        std::swap(qa, qb);
-        std::swap(ia, ib);
-      }
-      q2 = qa;
-      items2 = ia;
     }
   }
   // P2 with the amortised block-end test when the escape-monotonicity precondition
@@ -638,12 +595,12 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   static const int occ_env = env_int("FRACTAL_P2_OCC", 0);
   const int occ_want = occ_env > 0 ? occ_env : (amort ? 3 : 2);
   const int occ2 = occ_want < occ ? occ_want : occ;
-  kern<<<(unsigned)(sm_count() * occ2), fr::kThreads, 0, s>>>(g, pal, jcr, jci, q2, items2);
+  kern<<<(unsigned)(sm_count() * occ2), fr::kThreads, 0, s>>>(g, pal, jcr, jci, q, items);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     // P2 resets the queue header when it finishes; if it never ran, reset it here so
     // the next call does not start from P1's stale tail
-    cudaMemsetAsync(qp, 0, 2 * sizeof(fr::ContQueue), s);
+    cudaMemsetAsync(qp, 0, sizeof(fr::ContQueue), s);
     return e;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
