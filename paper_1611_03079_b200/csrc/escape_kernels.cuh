@@ -479,7 +479,7 @@ __device__ __forceinline__ int fast_vote_loop_f32<4>(float& x, float& y, int& cn
   "setp.le.and.f32 pa, m1, 0f41800000, pa;\n\t"      \
   "setp.le.and.f32 pb, m2, 0f41800000, pb;\n\t"      \
   "@pa add.s32 %2, %2, 1;\n\t"                       \
-  "@pb add.s32 %7, %7, 1;\n\t"                       \
+  FR_COUNT_B                                         \
   "mov.b64 {n1, n2}, yy;\n\t"                        \
   "neg.f32 n1, n1;\n\t"                              \
   "neg.f32 n2, n2;\n\t"                              \
@@ -490,6 +490,22 @@ __device__ __forceinline__ int fast_vote_loop_f32<4>(float& x, float& y, int& cn
 
 #ifndef FR_FFMA2
 #define FR_FFMA2 1  // 0: the scalar two-orbit loop (same-box A/B)
+#endif
+// FR_FCOUNT: the second orbit's count kept as a float and incremented with a predicated
+// FADD, which issues to the FMA pipe, instead of an IADD on the ALU pipe -- the packed
+// loop is ALU-bound, so this moves one instruction per iteration to
+// the pipe with room.  Exact: counts <= 65535 < 2^24.
+#ifndef FR_FCOUNT
+#define FR_FCOUNT 0
+#endif
+#if FR_FCOUNT
+#define FR_COUNT_B "@pb add.f32 cbf, cbf, 0f3F800000;\n\t"
+#define FR_COUNT_B_DECL ".reg .f32 cbf;\n\tcvt.rn.f32.s32 cbf, %7;\n\t"
+#define FR_COUNT_B_OUT "cvt.rzi.s32.f32 %7, cbf;\n\t"
+#else
+#define FR_COUNT_B "@pb add.s32 %7, %7, 1;\n\t"
+#define FR_COUNT_B_DECL ""
+#define FR_COUNT_B_OUT ""
 #endif
 
 template <int K>
@@ -509,7 +525,7 @@ __device__ __forceinline__ int fast_vote_loop2x_f32(float& x, float& y, int& cnt
   if constexpr (K == 1) {
     asm volatile(
         "{\n\t.reg .pred pa, pb, pm;\n\t.reg .b64 X, Y, CR, CI, HALF, yy, m, nyy, t;\n\t"
-        ".reg .f32 m1, m2, n1, n2;\n\t"
+        ".reg .f32 m1, m2, n1, n2;\n\t" FR_COUNT_B_DECL
         "mov.b64 X, {%0, %5};\n\tmov.b64 Y, {%1, %6};\n\t"
         "mov.b64 CR, {%12, %14};\n\tmov.b64 CI, {%13, %15};\n\t"
         "mov.b64 HALF, {0f3F000000, 0f3F000000};\n\t"
@@ -523,14 +539,14 @@ __device__ __forceinline__ int fast_vote_loop2x_f32(float& x, float& y, int& cnt
         "@pm bra FR_X1B_LOOP;\n"
         "FR_X1B_DONE:\n\t"
         "mov.b64 {%0, %5}, X;\n\tmov.b64 {%1, %6}, Y;\n\t"
-        "selp.u32 %3, 1, 0, pa;\n\tselp.u32 %8, 1, 0, pb;\n\t}"
+        FR_COUNT_B_OUT "selp.u32 %3, 1, 0, pa;\n\tselp.u32 %8, 1, 0, pb;\n\t}"
         : "+f"(x), "+f"(y), "+r"(cnt), "+r"(alive), "=r"(n), "+f"(x2), "+f"(y2), "+r"(cnt2),
           "+r"(alive2)
         : "r"(kfull), "r"(0), "r"(0), "f"(cr2), "f"(ci2), "f"(cr2b), "f"(ci2b));
   } else if constexpr (K == 4) {
     asm volatile(
         "{\n\t.reg .pred pa, pb, pm;\n\t.reg .b64 X, Y, CR, CI, HALF, yy, m, nyy, t;\n\t"
-        ".reg .f32 m1, m2, n1, n2;\n\t"
+        ".reg .f32 m1, m2, n1, n2;\n\t" FR_COUNT_B_DECL
         "mov.b64 X, {%0, %5};\n\tmov.b64 Y, {%1, %6};\n\t"
         "mov.b64 CR, {%12, %14};\n\tmov.b64 CI, {%13, %15};\n\t"
         "mov.b64 HALF, {0f3F000000, 0f3F000000};\n\t"
@@ -544,14 +560,14 @@ __device__ __forceinline__ int fast_vote_loop2x_f32(float& x, float& y, int& cnt
         "@pm bra FR_X4B_LOOP;\n"
         "FR_X4B_DONE:\n\t"
         "mov.b64 {%0, %5}, X;\n\tmov.b64 {%1, %6}, Y;\n\t"
-        "selp.u32 %3, 1, 0, pa;\n\tselp.u32 %8, 1, 0, pb;\n\t}"
+        FR_COUNT_B_OUT "selp.u32 %3, 1, 0, pa;\n\tselp.u32 %8, 1, 0, pb;\n\t}"
         : "+f"(x), "+f"(y), "+r"(cnt), "+r"(alive), "=r"(n), "+f"(x2), "+f"(y2), "+r"(cnt2),
           "+r"(alive2)
         : "r"(kfull), "r"(0), "r"(0), "f"(cr2), "f"(ci2), "f"(cr2b), "f"(ci2b));
   } else {
     asm volatile(
         "{\n\t.reg .pred pa, pb, pm;\n\t.reg .b64 X, Y, CR, CI, HALF, yy, m, nyy, t;\n\t"
-        ".reg .f32 m1, m2, n1, n2;\n\t"
+        ".reg .f32 m1, m2, n1, n2;\n\t" FR_COUNT_B_DECL
         "mov.b64 X, {%0, %5};\n\tmov.b64 Y, {%1, %6};\n\t"
         "mov.b64 CR, {%12, %14};\n\tmov.b64 CI, {%13, %15};\n\t"
         "mov.b64 HALF, {0f3F000000, 0f3F000000};\n\t"
@@ -565,7 +581,7 @@ __device__ __forceinline__ int fast_vote_loop2x_f32(float& x, float& y, int& cnt
         "@pm bra FR_X2B_LOOP;\n"
         "FR_X2B_DONE:\n\t"
         "mov.b64 {%0, %5}, X;\n\tmov.b64 {%1, %6}, Y;\n\t"
-        "selp.u32 %3, 1, 0, pa;\n\tselp.u32 %8, 1, 0, pb;\n\t}"
+        FR_COUNT_B_OUT "selp.u32 %3, 1, 0, pa;\n\tselp.u32 %8, 1, 0, pb;\n\t}"
         : "+f"(x), "+f"(y), "+r"(cnt), "+r"(alive), "=r"(n), "+f"(x2), "+f"(y2), "+r"(cnt2),
           "+r"(alive2)
         : "r"(kfull), "r"(0), "r"(0), "f"(cr2), "f"(ci2), "f"(cr2b), "f"(ci2b));
