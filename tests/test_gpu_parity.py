@@ -601,6 +601,55 @@ def test_side_stream_and_launch_count(fr):
     assert 2 <= fr.launch_count() - before <= 6
 
 
+def test_concurrent_host_threads_and_streams(fr):
+    """Reentrancy (include/fractal.h "Async"): four host threads, each on its own CUDA
+    stream, render heavy-tailed frames (P1 + P2 with their per-stream queue and survivor
+    buffer), paths (SX) and refill / amortised frames at the same time, several rounds;
+    every result equals the same render done alone on the default stream."""
+    import threading
+    c3 = -0.7269 + 0.1889j
+    win = W.julia_window(640, 360)
+    mwin = W.Window(-0.3 + 0.1j, 0.4, 0.225)
+    cs = W.circle_path(24)
+    jobs = [("twophase", lambda out: fr.julia_render_ex(c3, win, 640, 360, 1000,
+                                                         fr.Mode.FP32_FAST, out=out)),
+            ("twophase64", lambda out: fr.julia_render_ex(c3, win, 640, 360, 1000,
+                                                           fr.Mode.FP64_FAST, out=out)),
+            ("path", lambda out: fr.julia_render_path(cs, win, 640, 360, 100,
+                                                      fr.Mode.FP32_FAST, out=out)),
+            ("amort", lambda out: fr.mandelbrot_param_map(mwin, 640, 360, 2000,
+                                                          fr.Mode.FP64_FAST, out=out))]
+    shapes = {"path": (24, 360, 640)}
+    ref = {}
+    for name, fn in jobs:
+        out = torch.empty(shapes.get(name, (360, 640)), dtype=torch.uint16, device="cuda")
+        fn(out)
+        torch.cuda.synchronize()
+        ref[name] = np16(out)
+    errors = []
+
+    def worker(name, fn):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for _ in range(4):
+                    out = torch.empty(shapes.get(name, (360, 640)), dtype=torch.uint16,
+                                      device="cuda")
+                    fn(out)
+                    st.synchronize()
+                    if not np.array_equal(np16(out), ref[name]):
+                        errors.append(name)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(f"{name}: {e!r}")
+
+    threads = [threading.Thread(target=worker, args=j) for j in jobs]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+
+
 # ------------------------------------------------------------------ NEXT-2: cardioid path
 def test_cardioid_path_frames_strict(fr):
     """The paper's own dynamic workload: Julia frames along the a = 3.9 cardioid
