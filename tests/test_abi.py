@@ -162,3 +162,41 @@ def test_rank_without_bands_is_a_noop(lib):
     assert lib.julia_render_ex(C, W, 64, 1, 100, 0, B._Bands(4, 3, 1), None, None, None, STREAM) == 0
     assert lib.mandelbrot_param_map(W, 64, 4, 100, 2, B._Bands(4, 2, 1), None, None, None, STREAM) == 0
     assert lib.fr_launch_count() == before
+
+
+def _build_c_demo(tmp_path):
+    """Compile examples/c_abi_demo.c (plain C11 against include/fractal.h, linked to
+    libfractal.so only) -- the C ABI without Python or torch."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    from paper_1611_03079_b200 import build
+    build.build()
+    exe = tmp_path / "c_abi_demo"
+    pkg = os.path.dirname(build.LIB)
+    subprocess.run([cc, "-std=c11", "-Wall", "-Wextra", "-Werror",
+                    "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "c_abi_demo.c"), "-L", pkg, "-lfractal",
+                    "-lm", f"-Wl,-rpath,{pkg}", "-Wl,--allow-shlib-undefined", "-o", str(exe)],
+                   check=True)
+    return exe
+
+
+def test_c_abi_demo_builds(tmp_path):
+    """The demo compiles warning-free and, without a GPU, fails cleanly with FR_ERR_CUDA
+    through fr_status_str (no crash, exit code 1)."""
+    import subprocess
+    exe = _build_c_demo(tmp_path)
+    try:
+        import torch
+        has_gpu = torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        has_gpu = False
+    if has_gpu:
+        pytest.skip("GPU present: the run is covered by the -m gpu test")
+    r = subprocess.run([str(exe), "8", "8", "2", "100", "1", str(tmp_path / "x.bin")],
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 1, (r.returncode, r.stdout, r.stderr)
+    assert "FR_ERR_CUDA" in r.stderr

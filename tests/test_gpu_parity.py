@@ -650,6 +650,30 @@ def test_concurrent_host_threads_and_streams(fr):
     assert not errors, errors
 
 
+def test_c_abi_demo_program(fr, tmp_path):
+    """examples/c_abi_demo.c: a plain C program renders cfg4-path frames through
+    julia_render_path_host (host output, no CUDA calls of its own); its file equals the
+    oracle frame by frame, strict and fast."""
+    import subprocess
+    import sys as _sys
+    _sys.path.insert(0, os.path.dirname(__file__))
+    from test_abi import _build_c_demo
+    exe = _build_c_demo(tmp_path)
+    w, h, n = 96, 54, 6
+    cs = W.circle_path(n)
+    win = W.julia_window(w, h)
+    for mode, fast in ((1, False), (0, True)):
+        out = tmp_path / f"counts{mode}.bin"
+        r = subprocess.run([str(exe), str(w), str(h), str(n), "100", str(mode), str(out)],
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        got = np.fromfile(out, dtype="<u2").reshape(n, h, w)
+        for k in range(n):
+            ref = oracle.julia(complex(cs[k]), win.center, win.half_w, win.half_h, w, h, 100,
+                               32, fast=fast)
+            np.testing.assert_array_equal(got[k], ref)
+
+
 # ------------------------------------------------------------------ NEXT-2: cardioid path
 def test_cardioid_path_frames_strict(fr):
     """The paper's own dynamic workload: Julia frames along the a = 3.9 cardioid
