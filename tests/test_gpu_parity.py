@@ -834,3 +834,50 @@ def test_graph_capture_contract(fr):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(np16(out), want_c)
     np.testing.assert_array_equal(rgba.cpu().numpy(), want_rgba)
+
+
+def test_graph_replays_of_self_resetting_kernels(fr):
+    """The queue of P1 + P2, kernel R's chunk counter and kernel A reset themselves at the
+    end of each launch, so a CUDA graph of them replays correctly any number of times
+    (include/fractal.h "Graphs").  And the round-1 review's use-after-free scenario: a
+    graph captured with a small survivor buffer still replays correctly after a larger
+    frame made the buffer grow on the same stream (outgrown buffers are kept alive)."""
+    side = torch.cuda.Stream()
+    c3 = -0.7269 + 0.1889j
+    w, h = 480, 270
+    win = W.julia_window(w, h)
+    mwin = W.Window(-0.3 + 0.1j, 0.4, 0.225)
+    pal = W.palette("classic")
+    out1 = torch.empty((h, w), dtype=torch.uint16, device="cuda")
+    rgba1 = torch.empty((h, w, 4), dtype=torch.uint8, device="cuda")
+    out2 = torch.empty((h, w), dtype=torch.uint16, device="cuda")
+    out3 = torch.empty((h, w), dtype=torch.uint16, device="cuda")
+
+    def frame():
+        fr.julia_render_ex(c3, win, w, h, 1000, fr.Mode.FP32_FAST, out=out1, palette=pal,
+                           out_rgba=rgba1)                                    # P1 + P2
+        fr.julia_render_ex(c3, win, w, h, 1000, fr.Mode.FP64_STRICT, out=out2)  # P1 + P2
+        fr.mandelbrot_param_map(mwin, w, h, 2000, fr.Mode.FP32_FAST, out=out3)  # kernel A
+
+    with torch.cuda.stream(side):
+        frame()  # eager first use on this stream: workspaces, queue, palette copy
+    torch.cuda.synchronize()
+    want = [np16(out1), rgba1.cpu().numpy(), np16(out2), np16(out3)]
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        frame()
+    # grow the survivor buffer of this stream with a larger eager frame
+    with torch.cuda.stream(side):
+        big = fr.julia_render_ex(c3, W.julia_window(1920, 1080), 1920, 1080, 1000,
+                                 fr.Mode.FP32_FAST)
+    torch.cuda.synchronize()
+    del big
+    for _ in range(12):
+        for t in (out1, out2, out3):
+            t.view(torch.int16).fill_(-1)
+        rgba1.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        got = [np16(out1), rgba1.cpu().numpy(), np16(out2), np16(out3)]
+        for a, b in zip(got, want):
+            np.testing.assert_array_equal(a, b)
