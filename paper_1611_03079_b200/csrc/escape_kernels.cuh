@@ -916,6 +916,9 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
 // amortised over the group), one frame at a time.
 // ----------------------------------------------------------------------------------
 constexpr int kTileWX = 64;
+#ifndef FR_SX_UNROLL  // unroll the frame loop of kernel SX by 4 (A/B knob)
+#define FR_SX_UNROLL 0
+#endif
 #ifndef FR_SX_K  // vote block of kernel SX (A/B knob)
 #define FR_SX_K 2  // same box: 2.629 vs 2.734 ms per bench step (profiles/r02/ab_sx_votek.txt)
 #endif
@@ -950,18 +953,25 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
   const bool vec = in1 && ((g.W & 1) == 0) && ((stride & 1) == 0) &&
                    (base_c % (2 * ES)) == 0 &&
                    (!COLOR || (reinterpret_cast<uintptr_t>(g.rgba) & 7) == 0);
-  for (int f = f0; f < f1; ++f) {
+  // one frame; TAIL: max_iter is not a multiple of the vote block (hoisted out of the
+  // frame loop: the per-frame checks of the tail cost instructions on every frame)
+  auto frame = [&](const int f, auto tail_tag) {
+    constexpr bool TAIL = decltype(tail_tag)::value;
     float x = re0, y = im, x2 = re1, y2 = im;
     unsigned alive = in0 ? 1u : 0u, alive2 = in1 ? 1u : 0u;
     int cnt = 0, cnt2 = 0;
     const float cr = cs.re[f], ci = cs.im[f];
     int n = fast_vote_loop2x_f32<FR_SX_K>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr,
                                           ci, kfull);
-    if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
-      for (; n < max_iter; ++n) {
-        Iter<float, false>::step(x, y, cr, ci, alive, cnt);
-        Iter<float, false>::step(x2, y2, cr, ci, alive2, cnt2);
+    if constexpr (TAIL) {
+      if (n == kfull && __any_sync(kFull, alive | alive2)) {
+        for (; n < max_iter; ++n) {
+          Iter<float, false>::step(x, y, cr, ci, alive, cnt);
+          Iter<float, false>::step(x2, y2, cr, ci, alive2, cnt2);
+        }
       }
+    } else {
+      (void)n;
     }
     if (vec) {
       if constexpr (ES == 2)
@@ -985,6 +995,17 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
     }
     outp += stride;
     if (COLOR) outc += stride;
+  };
+  if (kfull == max_iter) {
+#if FR_SX_UNROLL
+#pragma unroll 4
+#else
+#pragma unroll 1
+#endif
+    for (int f = f0; f < f1; ++f) frame(f, std::false_type{});
+  } else {
+#pragma unroll 1
+    for (int f = f0; f < f1; ++f) frame(f, std::true_type{});
   }
 }
 
