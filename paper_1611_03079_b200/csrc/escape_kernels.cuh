@@ -43,13 +43,15 @@ constexpr unsigned kFull = 0xffffffffu;
 // ----------------------------------------------------------------------------------
 // Parameters (passed by value; the path chunk's C values ride in param space).
 // ----------------------------------------------------------------------------------
+// Colours are RGBA bytes packed in 32-bit words (R in the low byte: the byte order of
+// an RGBA image in memory), so a colour moves and selects as one register.
 struct Palette {
-  uchar4 e[256];
-  uchar4 interior;
+  uint32_t e[256];
+  uint32_t interior;
   uint32_t n;      // entries, 2..256
   uint32_t magic;  // ceil(2^32 / n): count mod n = c - n * umulhi(c, magic) for c < 2^16
-  const uchar4* dev;  // the n entries in device memory (short-lived CTAs read it through
-                      // L1 instead of staging e[] in shared memory behind a CTA barrier)
+  const uint32_t* dev;  // the n entries in device memory (short-lived CTAs read it through
+                        // L1 instead of staging e[] in shared memory behind a CTA barrier)
 };
 
 struct Geom {
@@ -63,7 +65,7 @@ struct Geom {
   int64_t frame_stride;  // rows * W
   uint16_t* counts;
   uint8_t* counts8;  // uint8 counts instead (max_iter <= 255; static kernel only), else null
-  uchar4* rgba;   // nullptr unless colour levels are fused
+  uint32_t* rgba;  // packed RGBA words; nullptr unless colour levels are fused
   int grid2d;     // kernels S/S2: tiles on grid x/y (frame groups on z), else tiles on x
 };
 
@@ -353,8 +355,8 @@ __device__ __forceinline__ T to_state(double v) {
 
 // Count -> colour level: interior if count == max_iter, else
 // palette[count mod n].
-__device__ __forceinline__ uchar4 colour_of(const uchar4* spal, const Palette& p, int cnt,
-                                            int max_iter) {
+__device__ __forceinline__ uint32_t colour_of(const uint32_t* spal, const Palette& p, int cnt,
+                                              int max_iter) {
   if (cnt == max_iter) return p.interior;
   const unsigned c = (unsigned)cnt;
   const unsigned q = __umulhi(c, p.magic);
@@ -365,14 +367,14 @@ __device__ __forceinline__ uchar4 colour_of(const uchar4* spal, const Palette& p
 // P1, P2S, P3): 24 bytes of kernel parameters instead of the 1.1-KB Palette (the launch
 // copies every parameter byte; it matters for small frames).
 struct PalRef {
-  const uchar4* dev;
-  uchar4 interior;
+  const uint32_t* dev;
+  uint32_t interior;
   uint32_t n;
   uint32_t magic;
 };
 
 // The same colour level from the device copy of the palette (read-only path).
-__device__ __forceinline__ uchar4 colour_dev(const PalRef& p, int cnt, int max_iter) {
+__device__ __forceinline__ uint32_t colour_dev(const PalRef& p, int cnt, int max_iter) {
   if (cnt == max_iter) return p.interior;
   const unsigned c = (unsigned)cnt;
   const unsigned q = __umulhi(c, p.magic);
@@ -730,7 +732,7 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
   static_assert(FN == 0 || (STRICT && !MANDEL), "map variants: strict Julia frames");
   static_assert(ES == 1 || ES == 2, "counts are uint16 (ES 2) or uint8 (ES 1)");
   using CountT = typename std::conditional<ES == 2, uint16_t, uint8_t>::type;
-  __shared__ uchar4 spal[COLOR ? 256 : 1];
+  __shared__ uint32_t spal[COLOR ? 256 : 1];
   int tx, ty, grp;
   tile_of(g, tx, ty, grp);
   if (COLOR) {
@@ -756,7 +758,7 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
   const int64_t pix0 = (int64_t)(frame0 + f0) * stride + (int64_t)ly * g.W + px;
   CountT* outp = (ES == 2 ? reinterpret_cast<CountT*>(g.counts)
                           : reinterpret_cast<CountT*>(g.counts8)) + pix0;
-  uchar4* outc = COLOR ? g.rgba + pix0 : nullptr;
+  uint32_t* outc = COLOR ? g.rgba + pix0 : nullptr;
   // Output sectors: with 8x4 warp tiles each 32-B sector of a count row is written half
   // by one warp and half by its neighbour, and over a frame group the two warps drift
   // apart in frames; a sector evicted from L2 half-written costs a DRAM read-modify-write
@@ -946,7 +948,7 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
   const int64_t pix0 = (int64_t)(frame0 + f0) * stride + (int64_t)ly * g.W + px;
   CountT* outp = (ES == 2 ? reinterpret_cast<CountT*>(g.counts)
                           : reinterpret_cast<CountT*>(g.counts8)) + pix0;
-  uchar4* outc = COLOR ? g.rgba + pix0 : nullptr;
+  uint32_t* outc = COLOR ? g.rgba + pix0 : nullptr;
   // one store for both counts when the pair is whole and aligned in every frame
   const uintptr_t base_c = ES == 2 ? reinterpret_cast<uintptr_t>(g.counts)
                                    : reinterpret_cast<uintptr_t>(g.counts8);
@@ -979,9 +981,8 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
       else
         *reinterpret_cast<uint16_t*>(outp) = (uint16_t)(cnt | (cnt2 << 8));
       if (COLOR) {
-        const uchar4 a = colour_dev(pal, cnt, max_iter), b = colour_dev(pal, cnt2, max_iter);
         *reinterpret_cast<uint2*>(outc) =
-            make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+            make_uint2(colour_dev(pal, cnt, max_iter), colour_dev(pal, cnt2, max_iter));
       }
     } else {
       if (in0) {
@@ -1358,7 +1359,7 @@ template <class T, bool STRICT, bool MANDEL, bool COLOR, int K, int TH, bool AMO
 __global__ void __launch_bounds__(kThreads)
 escape_cont_kernel(const Geom g, const Palette pal, const T jcr, const T jci, ContQueue* q,
                    const QItem<T>* items) {
-  __shared__ uchar4 spal[COLOR ? 256 : 1];
+  __shared__ uint32_t spal[COLOR ? 256 : 1];
   if (COLOR) {
     spal[threadIdx.x] = pal.e[threadIdx.x];
     __syncthreads();
@@ -1869,7 +1870,7 @@ template <class T, bool STRICT, bool MANDEL, bool COLOR, bool AMORT, int K, int 
 __global__ void __launch_bounds__(kThreads)
 escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, Workspace* ws,
                      unsigned n_chunks, unsigned chunks_per_cta) {
-  __shared__ uchar4 spal[COLOR ? 256 : 1];
+  __shared__ uint32_t spal[COLOR ? 256 : 1];
   __shared__ T tre[kThreads / 32][kTileW];
   __shared__ T tim[kThreads / 32][kTileH];
   __shared__ unsigned s_next;  // CTA-local chunk source (chunks_per_cta > 0)
@@ -2043,18 +2044,15 @@ escape_refill_kernel(const Geom g, const Palette pal, const T jcr, const T jci, 
 // ----------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
 colorize_kernel(const uint16_t* __restrict__ counts, int64_t n_pixels, int max_iter,
-                const Palette pal, uchar4* __restrict__ rgba) {
-  __shared__ uchar4 spal[256];
+                const Palette pal, uint32_t* __restrict__ rgba) {
+  __shared__ uint32_t spal[256];
   spal[threadIdx.x] = pal.e[threadIdx.x];
   __syncthreads();
   const int64_t groups = n_pixels >> 3;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const uint4* __restrict__ c8 = reinterpret_cast<const uint4*>(counts);
   uint4* __restrict__ o8 = reinterpret_cast<uint4*>(rgba);
-  auto pack = [&](uint32_t w16) {
-    const uchar4 a = colour_of(spal, pal, (int)(w16 & 0xffffu), max_iter);
-    return (uint32_t)a.x | ((uint32_t)a.y << 8) | ((uint32_t)a.z << 16) | ((uint32_t)a.w << 24);
-  };
+  auto pack = [&](uint32_t w16) { return colour_of(spal, pal, (int)(w16 & 0xffffu), max_iter); };
   auto emit = [&](int64_t i, const uint4 v) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     uint32_t o[8];
@@ -2087,8 +2085,8 @@ colorize_kernel(const uint16_t* __restrict__ counts, int64_t n_pixels, int max_i
 // Unaligned fallback (pointers not 16-byte aligned): one pixel per thread-step.
 __global__ void __launch_bounds__(kThreads)
 colorize_scalar_kernel(const uint16_t* __restrict__ counts, int64_t n_pixels, int max_iter,
-                       const Palette pal, uchar4* __restrict__ rgba) {
-  __shared__ uchar4 spal[256];
+                       const Palette pal, uint32_t* __restrict__ rgba) {
+  __shared__ uint32_t spal[256];
   spal[threadIdx.x] = pal.e[threadIdx.x];
   __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;

@@ -83,14 +83,19 @@ int64_t local_rows(int32_t height, fr_bands b) {
   return rows;
 }
 
+// RGBA bytes as one little-endian word (R in the low byte: the in-memory byte order)
+uint32_t rgba_word(uint8_t r, uint8_t g, uint8_t b, uint8_t a) {
+  return (uint32_t)r | ((uint32_t)g << 8) | ((uint32_t)b << 16) | ((uint32_t)a << 24);
+}
+
 fr_status make_palette(const fr_palette* pal, fr::Palette* out) {
   std::memset(out, 0, sizeof(*out));
   if (!pal) return FR_OK;
   if (!pal->rgba || pal->n < 2 || pal->n > 256) return FR_ERR_INVALID_ARG;
   for (int i = 0; i < pal->n; ++i)
-    out->e[i] = make_uchar4(pal->rgba[4 * i], pal->rgba[4 * i + 1], pal->rgba[4 * i + 2],
+    out->e[i] = rgba_word(pal->rgba[4 * i], pal->rgba[4 * i + 1], pal->rgba[4 * i + 2],
                             pal->rgba[4 * i + 3]);
-  out->interior = make_uchar4(pal->interior[0], pal->interior[1], pal->interior[2],
+  out->interior = rgba_word(pal->interior[0], pal->interior[1], pal->interior[2],
                               pal->interior[3]);
   out->n = (uint32_t)pal->n;
   out->magic = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)pal->n - 1) / (uint64_t)pal->n);
@@ -102,8 +107,8 @@ fr_status make_palette(const fr_palette* pal, fr::Palette* out) {
 // the palette in shared memory behind a CTA barrier.  A new palette is uploaded once,
 // outside any graph capture (like the workspaces).
 struct DevPalette {
-  std::vector<uchar4> entries;
-  uchar4* ptr;
+  std::vector<uint32_t> entries;
+  uint32_t* ptr;
 };
 std::mutex g_pal_mutex;
 std::map<std::pair<int, uint64_t>, std::vector<DevPalette>> g_pal_dev;
@@ -115,8 +120,7 @@ cudaError_t device_palette(fr::Palette& p, cudaStream_t s) {
   if (p.n == 0) return cudaSuccess;
   uint64_t h = 1469598103934665603ull;  // FNV-1a over the entries
   for (uint32_t i = 0; i < p.n; ++i) {
-    const uchar4 v = p.e[i];
-    for (unsigned char b : {v.x, v.y, v.z, v.w}) h = (h ^ b) * 1099511628211ull;
+    for (int k = 0; k < 4; ++k) h = (h ^ ((p.e[i] >> (8 * k)) & 0xffu)) * 1099511628211ull;
   }
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -125,19 +129,19 @@ cudaError_t device_palette(fr::Palette& p, cudaStream_t s) {
   auto& bucket = g_pal_dev[std::make_pair(dev, h)];
   for (const DevPalette& d : bucket) {
     if (d.entries.size() == p.n &&
-        std::memcmp(d.entries.data(), p.e, p.n * sizeof(uchar4)) == 0) {
+        std::memcmp(d.entries.data(), p.e, p.n * sizeof(uint32_t)) == 0) {
       p.dev = d.ptr;
       return cudaSuccess;
     }
   }
   if (capturing(s)) return cudaErrorStreamCaptureUnsupported;
-  uchar4* ptr = nullptr;
-  e = cudaMalloc(&ptr, p.n * sizeof(uchar4));
+  uint32_t* ptr = nullptr;
+  e = cudaMalloc(&ptr, p.n * sizeof(uint32_t));
   if (e != cudaSuccess) return e;
   // stream-ordered upload on the caller's stream, then wait for it: the copy is shared
   // by later calls on any stream, which are not ordered after `s` (one-time cost)
-  bucket.push_back(DevPalette{std::vector<uchar4>(p.e, p.e + p.n), ptr});
-  e = cudaMemcpyAsync(ptr, bucket.back().entries.data(), p.n * sizeof(uchar4),
+  bucket.push_back(DevPalette{std::vector<uint32_t>(p.e, p.e + p.n), ptr});
+  e = cudaMemcpyAsync(ptr, bucket.back().entries.data(), p.n * sizeof(uint32_t),
                       cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
@@ -177,7 +181,7 @@ fr::Geom make_geom(fr_window win, int32_t width, int32_t height, int32_t max_ite
   g.frame_stride = rows * (int64_t)width;
   g.counts = counts;
   g.counts8 = nullptr;
-  g.rgba = reinterpret_cast<uchar4*>(rgba);
+  g.rgba = reinterpret_cast<uint32_t*>(rgba);
   g.grid2d = 0;
   return g;
 }
@@ -1003,7 +1007,7 @@ fr_status colorize(const uint16_t* counts, int64_t n_pixels, int32_t max_iter,
   const int64_t cap = (int64_t)sms * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  uchar4* o = reinterpret_cast<uchar4*>(out_rgba);
+  uint32_t* o = reinterpret_cast<uint32_t*>(out_rgba);
   if (aligned)
     fr::colorize_kernel<<<(unsigned)blocks, fr::kThreads, 0, stream>>>(counts, n_pixels,
                                                                         max_iter, p, o);
