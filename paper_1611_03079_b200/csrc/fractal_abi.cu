@@ -525,7 +525,9 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
       if (p1ks == 4 && p1pre == 8)
         kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 4, 8>;
       if (p1ks == 8 && p1pre == 8)
-        kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 8, 8>;
+        kern1 = vote_k() == 2 && sizeof(T) == 4
+                    ? fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 8, 8, 2>
+                    : fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 8, 8>;
       if (p1ks == 4 && p1pre == 16)
         kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 4, 16>;
       if (p1ks == 8 && p1pre == 16)
