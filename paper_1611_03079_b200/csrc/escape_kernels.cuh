@@ -97,12 +97,17 @@ struct CList {
 // Region-covering map, reading c-3: pixel centres, row 0 at the top, binary64
 // with each operation separately rounded (explicit _rn intrinsics: no contraction).
 // ----------------------------------------------------------------------------------
+// The integer k = 2 px + 1 - W (H - 1 - 2 gy) is formed directly in binary64: every
+// operand and every intermediate is an integer below 2^33, so the doubling and the
+// addition are exact and k is the same double as the integer computed in 64 bits and
+// converted (a shorter dependency chain in the kernels' prologue than 64-bit integer
+// arithmetic; no fused operation, so the strict kernels' no-FMA guard still holds).
 __device__ __forceinline__ double pixel_re(const Geom& g, int px) {
-  const double k = (double)(2 * (long long)px + 1 - g.W);
+  const double k = __dadd_rn(__dmul_rn(2.0, (double)px), (double)(1 - g.W));
   return __dadd_rn(g.cx, __dmul_rn(k, g.hx));
 }
 __device__ __forceinline__ double pixel_im(const Geom& g, int gy) {
-  const double k = (double)((long long)g.H - 1 - 2 * (long long)gy);
+  const double k = __dadd_rn((double)(g.H - 1), __dmul_rn(-2.0, (double)gy));
   return __dadd_rn(g.cy, __dmul_rn(k, g.hy));
 }
 
