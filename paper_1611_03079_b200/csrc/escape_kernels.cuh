@@ -6,8 +6,8 @@
 // Kernels (DESIGN.md §5 has the dispatch table and the measurements):
 //   escape_tile_kernel    S   static tiles; frame groups of a C-path, two frames per lane
 //   escape_tile2_kernel   S2  one fp32 frame, two pixels per thread
-//   escape_budget_kernel  P1  heavy-tailed frames: static pass up to a budget, survivors
-//                             appended to a queue
+//   escape_budget_kernel  P1  heavy-tailed frames: static pass up to a budget (fp32 fast:
+//                             packed amortised sub-blocks), survivors appended to a queue
 //   escape_cont_kernel    P2  persistent lane refill over P1's survivors; fast modes with
 //                             |C| <= 1.989 amortise the escape test (block-end test,
 //                             checkpointed sub-blocks, exact replay of one sub-block)
@@ -18,9 +18,10 @@
 //   escape_cont2s_kernel  P2S experimental packed P2 (two orbits per lane, stashes, batched
 //                             in-warp replay; off by default)
 //   colorize_kernel           count -> RGBA colour levels (HBM-bound)
-// All iteration goes through Iter<T, STRICT>::step / core or the PTX vote loops, which
-// implement the same operation sequences (FAST: doubled state, FMA-contracted; STRICT:
-// reading c-9's sequence), so counts do not depend on the kernel.
+// All iteration goes through Iter<T, STRICT>::step / core, the packed fast_core2 and the
+// PTX vote loops, which implement the same operation sequences (FAST: doubled state,
+// FMA-contracted -- packed FFMA2 halves are separately rounded fused ops; STRICT:
+// reading c-9's sequence, scalar), so counts do not depend on the kernel.
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -369,7 +370,7 @@ __device__ __forceinline__ uint32_t colour_of(const uint32_t* spal, const Palett
 }
 
 // What the kernels that read colours from the device copy need of a palette (S2, SX,
-// P1, P2S, P3): 24 bytes of kernel parameters instead of the 1.1-KB Palette (the launch
+// P1, P2S): 24 bytes of kernel parameters instead of the 1.1-KB Palette (the launch
 // copies every parameter byte; it matters for small frames).
 struct PalRef {
   const uint32_t* dev;
