@@ -596,6 +596,74 @@ __device__ __forceinline__ int fast_vote_loop2x_f32(float& x, float& y, int& cnt
   }
   return n;
 }
+// Kernel SX's frame loop (§5.3c).  Every frame of a C-path starts its pixels from the
+// same state (X0, Y0), so the first iteration's squares, its escape test and
+// T0 = X0*X0 - Y0*Y0 do not depend on the frame: sx_pre computes them once per lane,
+// and per frame only Y1 = fma(X0, Y0, CI) and X1 = fma(T0, 1/2, CR) remain of the first
+// iteration; the second iteration follows, then the K = 2 vote loop is entered at its
+// vote.  Same operations on the same values as fast_vote_loop2x_f32<2>: bit-identical.
+struct SxPre {
+  uint64_t X0, Y0, T0;  // packed pairs (x, x2), (y, y2), (t, t2) of the first iteration
+  int c0, c1;           // counts after the first iteration (1 = passed its escape test)
+};
+__device__ __forceinline__ SxPre sx_pre(float re0, float re1, float im, bool in0, bool in1) {
+  SxPre p;
+  asm("{\n\t.reg .pred pa, pb;\n\t.reg .b64 yy, m, nyy;\n\t.reg .f32 m1, m2, n1, n2;\n\t"
+      "mov.b64 %0, {%5, %6};\n\tmov.b64 %1, {%7, %7};\n\t"
+      "mul.rn.f32x2 yy, %1, %1;\n\t"
+      "fma.rn.f32x2 m, %0, %0, yy;\n\t"
+      "mov.b64 {m1, m2}, m;\n\t"
+      "setp.ne.u32 pa, %8, 0;\n\tsetp.ne.u32 pb, %9, 0;\n\t"
+      "setp.le.and.f32 pa, m1, 0f41800000, pa;\n\t"
+      "setp.le.and.f32 pb, m2, 0f41800000, pb;\n\t"
+      "selp.u32 %3, 1, 0, pa;\n\tselp.u32 %4, 1, 0, pb;\n\t"
+      "mov.b64 {n1, n2}, yy;\n\tneg.f32 n1, n1;\n\tneg.f32 n2, n2;\n\t"
+      "mov.b64 nyy, {n1, n2};\n\t"
+      "fma.rn.f32x2 %2, %0, %0, nyy;\n\t}"
+      : "=l"(p.X0), "=l"(p.Y0), "=l"(p.T0), "=r"(p.c0), "=r"(p.c1)
+      : "f"(re0), "f"(re1), "f"(im), "r"((unsigned)in0), "r"((unsigned)in1));
+  return p;
+}
+#define FR_SX_STEP                                   \
+  "mul.rn.f32x2 yy, Y, Y;\n\t"                       \
+  "fma.rn.f32x2 m, X, X, yy;\n\t"                    \
+  "mov.b64 {m1, m2}, m;\n\t"                         \
+  "setp.le.and.f32 pa, m1, 0f41800000, pa;\n\t"      \
+  "setp.le.and.f32 pb, m2, 0f41800000, pb;\n\t"      \
+  "@pa add.s32 %0, %0, 1;\n\t"                       \
+  "@pb add.s32 %1, %1, 1;\n\t"                       \
+  "mov.b64 {n1, n2}, yy;\n\t"                        \
+  "neg.f32 n1, n1;\n\t"                              \
+  "neg.f32 n2, n2;\n\t"                              \
+  "mov.b64 nyy, {n1, n2};\n\t"                       \
+  "fma.rn.f32x2 t, X, X, nyy;\n\t"                   \
+  "fma.rn.f32x2 Y, X, Y, CI;\n\t"                    \
+  "fma.rn.f32x2 X, t, HALF, CR;\n\t"
+// one frame: counts of the lane's two pixels for C = (cr, ci); kfull even and >= 2
+__device__ __forceinline__ void sx_frame(const SxPre& p, float cr, float ci, int kfull,
+                                         int& cnt, int& cnt2) {
+  asm volatile(
+      "{\n\t.reg .pred pa, pb, pm;\n\t.reg .b64 X, Y, CR, CI, HALF, yy, m, nyy, t;\n\t"
+      ".reg .f32 m1, m2, n1, n2;\n\t.reg .s32 n;\n\t"
+      "mov.b64 CR, {%5, %5};\n\tmov.b64 CI, {%6, %6};\n\t"
+      "mov.b64 HALF, {0f3F000000, 0f3F000000};\n\t"
+      "mov.u32 %0, %7;\n\tmov.u32 %1, %8;\n\t"
+      "setp.ne.u32 pa, %7, 0;\n\tsetp.ne.u32 pb, %8, 0;\n\t"
+      "fma.rn.f32x2 Y, %2, %3, CI;\n\t"
+      "fma.rn.f32x2 X, %4, HALF, CR;\n\t" FR_SX_STEP
+      "mov.u32 n, 2;\n\t"
+      "bra.uni FR_SXF_CHECK;\n"
+      "FR_SXF_LOOP:\n\t" FR_SX_STEP FR_SX_STEP
+      "add.s32 n, n, 2;\n"
+      "FR_SXF_CHECK:\n\t"
+      "or.pred pm, pa, pb;\n\t"
+      "vote.sync.any.pred pm, pm, 0xffffffff;\n\t"
+      "setp.lt.and.s32 pm, n, %9, pm;\n\t"
+      "@pm bra FR_SXF_LOOP;\n\t}"
+      : "=r"(cnt), "=r"(cnt2)
+      : "l"(p.X0), "l"(p.Y0), "l"(p.T0), "f"(cr), "f"(ci), "r"(p.c0), "r"(p.c1), "r"(kfull));
+}
+#undef FR_SX_STEP
 #undef FR_FAST_STEP2X
 
 template <>
@@ -930,7 +998,12 @@ constexpr int kTileWX = 64;
 #ifndef FR_SX_K  // vote block of kernel SX (A/B knob)
 #define FR_SX_K 2  // same box: 2.629 vs 2.734 ms per bench step (profiles/r02/ab_sx_votek.txt)
 #endif
-template <int NC, int ES, bool COLOR>
+#ifndef FR_SX_PEEL  // first iteration hoisted out of the frame loop (A/B knob)
+#define FR_SX_PEEL 1
+#endif
+// VEC (host-checked): even width and frame stride, aligned outputs -- both pixels of a
+// lane are in or out together and every pair store is aligned
+template <int NC, int ES, bool COLOR, bool VEC>
 __global__ void __launch_bounds__(kThreads)
 escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, int frame0,
                     int n_frames, int fpc) {
@@ -958,17 +1031,22 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
   // one store for both counts when the pair is whole and aligned in every frame
   const uintptr_t base_c = ES == 2 ? reinterpret_cast<uintptr_t>(g.counts)
                                    : reinterpret_cast<uintptr_t>(g.counts8);
-  const bool vec = in1 && ((g.W & 1) == 0) && ((stride & 1) == 0) &&
-                   (base_c % (2 * ES)) == 0 &&
-                   (!COLOR || (reinterpret_cast<uintptr_t>(g.rgba) & 7) == 0);
+  const bool vec = VEC || (in1 && ((g.W & 1) == 0) && ((stride & 1) == 0) &&
+                           (base_c % (2 * ES)) == 0 &&
+                           (!COLOR || (reinterpret_cast<uintptr_t>(g.rgba) & 7) == 0));
   // one frame; TAIL: max_iter is not a multiple of the vote block (hoisted out of the
   // frame loop: the per-frame checks of the tail cost instructions on every frame)
+  const SxPre pre = sx_pre(re0, re1, im, in0, in1);
   auto frame = [&](const int f, auto tail_tag) {
-    constexpr bool TAIL = decltype(tail_tag)::value;
+    constexpr bool TAIL = decltype(tail_tag)::value == 1;
+    constexpr bool PEEL = decltype(tail_tag)::value == 2;
     float x = re0, y = im, x2 = re1, y2 = im;
     unsigned alive = in0 ? 1u : 0u, alive2 = in1 ? 1u : 0u;
     int cnt = 0, cnt2 = 0;
     const float cr = cs.re[f], ci = cs.im[f];
+    if constexpr (PEEL) {
+      sx_frame(pre, cr, ci, kfull, cnt, cnt2);
+    } else {
     int n = fast_vote_loop2x_f32<FR_SX_K>(x, y, cnt, alive, x2, y2, cnt2, alive2, cr, ci, cr,
                                           ci, kfull);
     if constexpr (TAIL) {
@@ -981,7 +1059,19 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
     } else {
       (void)n;
     }
-    if (vec) {
+    }
+    if (VEC) {
+      if (in0) {
+        if constexpr (ES == 2)
+          *reinterpret_cast<uint32_t*>(outp) = (uint32_t)cnt | ((uint32_t)cnt2 << 16);
+        else
+          *reinterpret_cast<uint16_t*>(outp) = (uint16_t)(cnt | (cnt2 << 8));
+        if (COLOR) {
+          *reinterpret_cast<uint2*>(outc) =
+              make_uint2(colour_dev(pal, cnt, max_iter), colour_dev(pal, cnt2, max_iter));
+        }
+      }
+    } else if (vec) {
       if constexpr (ES == 2)
         *reinterpret_cast<uint32_t*>(outp) = (uint32_t)cnt | ((uint32_t)cnt2 << 16);
       else
@@ -1003,16 +1093,19 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
     outp += stride;
     if (COLOR) outc += stride;
   };
-  if (kfull == max_iter) {
+  if (FR_SX_PEEL && FR_SX_K == 2 && kfull == max_iter && kfull >= 2) {
+#pragma unroll 1
+    for (int f = f0; f < f1; ++f) frame(f, std::integral_constant<int, 2>{});
+  } else if (kfull == max_iter) {
 #if FR_SX_UNROLL
 #pragma unroll 4
 #else
 #pragma unroll 1
 #endif
-    for (int f = f0; f < f1; ++f) frame(f, std::false_type{});
+    for (int f = f0; f < f1; ++f) frame(f, std::integral_constant<int, 0>{});
   } else {
 #pragma unroll 1
-    for (int f = f0; f < f1; ++f) frame(f, std::true_type{});
+    for (int f = f0; f < f1; ++f) frame(f, std::integral_constant<int, 1>{});
   }
 }
 

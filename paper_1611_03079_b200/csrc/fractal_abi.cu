@@ -232,12 +232,18 @@ cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr:
       const int fpcx = fpc_env > 0 ? fpc : (n_frames < 64 ? n_frames : 64);
       const dim3 gridx =
           tile_grid(gx, (g.rows + fr::kTileH - 1) / fr::kTileH, (n_frames + fpcx - 1) / fpcx);
-      if (g.counts8 != nullptr)
-        fr::escape_pathx_kernel<NC, 1, COLOR>
-            <<<gridx, fr::kThreads, 0, s>>>(gx, pal_ref(pal), cs, frame0, n_frames, fpcx);
-      else
-        fr::escape_pathx_kernel<NC, 2, COLOR>
-            <<<gridx, fr::kThreads, 0, s>>>(gx, pal_ref(pal), cs, frame0, n_frames, fpcx);
+      // VEC: both pixels of every lane pair in or out together, pair stores aligned
+      const int es = g.counts8 != nullptr ? 1 : 2;
+      const uintptr_t base_c = g.counts8 != nullptr ? reinterpret_cast<uintptr_t>(g.counts8)
+                                                    : reinterpret_cast<uintptr_t>(g.counts);
+      const bool vec = (g.W % 2) == 0 && (g.frame_stride % 2) == 0 && base_c % (2 * es) == 0 &&
+                       (!COLOR || reinterpret_cast<uintptr_t>(g.rgba) % 8 == 0);
+      auto kx = g.counts8 != nullptr
+                    ? (vec ? fr::escape_pathx_kernel<NC, 1, COLOR, true>
+                           : fr::escape_pathx_kernel<NC, 1, COLOR, false>)
+                    : (vec ? fr::escape_pathx_kernel<NC, 2, COLOR, true>
+                           : fr::escape_pathx_kernel<NC, 2, COLOR, false>);
+      kx<<<gridx, fr::kThreads, 0, s>>>(gx, pal_ref(pal), cs, frame0, n_frames, fpcx);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return cudaGetLastError();
     }
