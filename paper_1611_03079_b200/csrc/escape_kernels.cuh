@@ -663,6 +663,63 @@ __device__ __forceinline__ void sx_frame(const SxPre& p, float cr, float ci, int
       : "=r"(cnt), "=r"(cnt2)
       : "l"(p.X0), "l"(p.Y0), "l"(p.T0), "f"(cr), "f"(ci), "r"(p.c0), "r"(p.c1), "r"(kfull));
 }
+#define FR_SX_STEP_C                                 \
+  "mul.rn.f32x2 yy, Y, Y;\n\t"                       \
+  "fma.rn.f32x2 m, X, X, yy;\n\t"                    \
+  "mov.b64 {m1, m2}, m;\n\t"                         \
+  "setp.le.and.f32 pa, m1, 0f41800000, pa;\n\t"      \
+  "setp.le.and.f32 pb, m2, 0f41800000, pb;\n\t"      \
+  "@pa add.s32 %%c0, %%c0, 1;\n\t"                   \
+  "@pb add.s32 %%c1, %%c1, 1;\n\t"                   \
+  "mov.b64 {n1, n2}, yy;\n\t"                        \
+  "neg.f32 n1, n1;\n\t"                              \
+  "neg.f32 n2, n2;\n\t"                              \
+  "mov.b64 nyy, {n1, n2};\n\t"                       \
+  "fma.rn.f32x2 t, X, X, nyy;\n\t"                   \
+  "fma.rn.f32x2 Y, X, Y, CI;\n\t"                    \
+  "fma.rn.f32x2 X, t, HALF, CR;\n\t"
+// The whole frame loop of kernel SX in one PTX block (uint16 counts, whole pairs, no
+// colour): per frame one shared-memory load of C, the hoisted first iteration, the vote
+// loop, one 4-byte store and the pointer bump.  cbase: shared-memory address of the
+// group's (cr, ci) pairs; out: the lane's pair address in the group's first frame.
+__device__ __forceinline__ void sx_frames_u16(const SxPre& p, uint32_t cbase, int nfr,
+                                              uint32_t* out, int64_t stride_bytes, int kfull,
+                                              bool in0) {
+  asm volatile(
+      "{\n\t.reg .pred pa, pb, pm, pin, pf;\n\t.reg .b64 X, Y, CR, CI, HALF, yy, m, nyy, t, P;\n\t"
+      ".reg .f32 m1, m2, n1, n2, cr, ci;\n\t.reg .s32 n, %%c0, %%c1, f;\n\t.reg .u32 v, ca;\n\t"
+      "mov.b64 HALF, {0f3F000000, 0f3F000000};\n\t"
+      "setp.ne.u32 pin, %10, 0;\n\t"
+      "mov.u64 P, %6;\n\tmov.u32 ca, %5;\n\tmov.u32 f, 0;\n"
+      "FR_SXA_FRAME:\n\t"
+      "ld.shared.v2.f32 {cr, ci}, [ca];\n\t"
+      "mov.b64 CR, {cr, cr};\n\tmov.b64 CI, {ci, ci};\n\t"
+      "mov.u32 %%c0, %3;\n\tmov.u32 %%c1, %4;\n\t"
+      "setp.ne.u32 pa, %3, 0;\n\tsetp.ne.u32 pb, %4, 0;\n\t"
+      "fma.rn.f32x2 Y, %0, %1, CI;\n\t"
+      "fma.rn.f32x2 X, %2, HALF, CR;\n\t" FR_SX_STEP_C
+      "mov.u32 n, 2;\n\t"
+      "bra.uni FR_SXA_CHECK;\n"
+      "FR_SXA_LOOP:\n\t" FR_SX_STEP_C FR_SX_STEP_C
+      "add.s32 n, n, 2;\n"
+      "FR_SXA_CHECK:\n\t"
+      "or.pred pm, pa, pb;\n\t"
+      "vote.sync.any.pred pm, pm, 0xffffffff;\n\t"
+      "setp.lt.and.s32 pm, n, %9, pm;\n\t"
+      "@pm bra FR_SXA_LOOP;\n\t"
+      "prmt.b32 v, %%c0, %%c1, 0x5410;\n\t"
+      "@pin st.global.u32 [P], v;\n\t"
+      "add.s64 P, P, %7;\n\t"
+      "add.u32 ca, ca, 8;\n\t"
+      "add.s32 f, f, 1;\n\t"
+      "setp.lt.s32 pf, f, %8;\n\t"
+      "@pf bra FR_SXA_FRAME;\n\t}"
+      :
+      : "l"(p.X0), "l"(p.Y0), "l"(p.T0), "r"(p.c0), "r"(p.c1), "r"(cbase), "l"(out),
+        "l"(stride_bytes), "r"(nfr), "r"(kfull), "r"((unsigned)in0)
+      : "memory");
+}
+#undef FR_SX_STEP_C
 #undef FR_SX_STEP
 #undef FR_FAST_STEP2X
 
@@ -1001,6 +1058,10 @@ constexpr int kTileWX = 64;
 #ifndef FR_SX_PEEL  // first iteration hoisted out of the frame loop (A/B knob)
 #define FR_SX_PEEL 1
 #endif
+#ifndef FR_SX_ASM  // the whole frame loop as one PTX block (uint16, no colour; A/B knob)
+#define FR_SX_ASM 1
+#endif
+constexpr int kSxChunk = 128;  // frames per shared-memory C chunk
 // VEC (host-checked): even width and frame stride, aligned outputs -- both pixels of a
 // lane are in or out together and every pair store is aligned
 template <int NC, int ES, bool COLOR, bool VEC>
@@ -1093,6 +1154,22 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
     outp += stride;
     if (COLOR) outc += stride;
   };
+  if constexpr (FR_SX_ASM && ES == 2 && !COLOR && VEC) {
+    if (FR_SX_PEEL && FR_SX_K == 2 && kfull == max_iter && kfull >= 2) {
+      // the frame loop in one PTX block, C staged in shared memory per chunk of frames
+      __shared__ float2 sc[kSxChunk];
+      for (int c0 = f0; c0 < f1; c0 += kSxChunk) {
+        const int nc = min(kSxChunk, f1 - c0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < nc; i += kThreads) sc[i] = make_float2(cs.re[c0 + i], cs.im[c0 + i]);
+        __syncthreads();
+        sx_frames_u16(pre, static_cast<uint32_t>(__cvta_generic_to_shared(sc)), nc,
+                      reinterpret_cast<uint32_t*>(outp), stride * 2, kfull, in0);
+        outp += (int64_t)nc * stride;
+      }
+      return;
+    }
+  }
   if (FR_SX_PEEL && FR_SX_K == 2 && kfull == max_iter && kfull >= 2) {
 #pragma unroll 1
     for (int f = f0; f < f1; ++f) frame(f, std::integral_constant<int, 2>{});
