@@ -307,7 +307,7 @@ def main():
     achieved = iters_per_step / (kavg * 1e-3) / 1e9
     roof = {"bound": "alu", "achieved": achieved, "peak": peak_gpix, "unit": "Gpixel-iter/s",
             "frac": achieved / peak_gpix, "traffic": None,
-            "kernel": "fr::escape_pathx_kernel<1024,2,false> (SX: C-path frames, FP32_FAST)",
+            "kernel": "fr::escape_pathx_kernel<1024,2,false,true> (SX: C-path frames, FP32_FAST, PTX frame loop)",
             "peak_basis": f"{SM_COUNT} SMs x {FP32_LANES_PER_SM} FP32 lanes x {f_max:.0f} MHz "
                           f"(MEASURED_PEAKS.json sm_max_mhz) / {ALG_OPS_PER_ITER} FMA-pipe ops "
                           "per pixel-iteration (DESIGN.md §5)",

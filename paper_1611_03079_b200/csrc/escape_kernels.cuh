@@ -14,7 +14,9 @@
 //   escape_refill_kernel  R / A  persistent lane refill over pixel chunks; A amortises
 //                             the escape test (block-end test + exact replay)
 //   escape_pathx_kernel   SX  C-path frames, FP32_FAST: two x-adjacent pixels per lane
-//                             (packed FFMA2 loop), whole-sector count stores
+//                             (packed FFMA2 loop), whole-sector count stores; the
+//                             frame-independent first iteration hoisted (sx_pre), the
+//                             uint16 frame loop as one PTX block (sx_frames_u16)
 //   escape_cont2s_kernel  P2S experimental packed P2 (two orbits per lane, stashes, batched
 //                             in-warp replay; off by default)
 //   colorize_kernel           count -> RGBA colour levels (HBM-bound)
