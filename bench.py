@@ -652,6 +652,57 @@ def extras(fr, W, torch):
     torch.cuda.empty_cache()
     res["colorize_hbm"] = colorize_bandwidth(fr, W, torch)
     res["cardioid_path"] = cardioid_path_rate(fr, W, torch, f_max)
+    res["fig4_maps"] = fig4_maps_rate(fr, W, torch, f_max)
+    return res
+
+
+# FP32-pipe operations per iteration of the Figure 4 maps' defining sequence (DESIGN.md
+# reading c-14; every operation separately rounded): z^4 + c = 7 MUL + 6 ADD/SUB (the
+# |Z|^2 test included); the rational map adds 8 MUL + 5 ADD/SUB and two IEEE divisions
+FIG4_OPS = {"Z4": 13, "Z4_RATIONAL": 26}
+
+
+def fig4_maps_rate(fr, W, torch, f_max):
+    """NEXT-3: Julia frames of z^4 + c and z^4 + (z^2+1)/(z^2-1) + c at 1080p,
+    C = FIG4_C, max_iter 100, FP32 (the maps run the strict sequence), through
+    julia_render_fn: both maps on the full view (real span 3; z^4 + c is a dust of
+    orbits <= 14 long there) and the rational map on the Figure 4 "zoom" window
+    (W.FIG4_ZOOM_*); rate against the FP32 pipe for the map's op count."""
+    res = {}
+    try:
+        out = torch.empty((H_PX, W_PX), dtype=torch.uint16, device="cuda")
+        full = W.julia_window(W_PX, H_PX, span_re=3.0)
+        zoom = W.julia_window(W_PX, H_PX, span_re=W.FIG4_ZOOM_SPAN, center=W.FIG4_ZOOM_CENTER)
+        for key, name, win in (("z4", "Z4", full), ("z4_rational", "Z4_RATIONAL", full),
+                               ("z4_rational_zoom", "Z4_RATIONAL", zoom)):
+            f = fr.Function[name]
+
+            def call():
+                fr.julia_render_fn(f, W.FIG4_C, win, W_PX, H_PX, MAX_ITER, fr.Mode.FP32_STRICT,
+                                   out=out)
+            call()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            reps = 20
+            a.record()
+            for _ in range(reps):
+                call()
+            b.record()
+            b.synchronize()
+            ms = a.elapsed_time(b) / reps
+            s = float((out.view(torch.int16).to(torch.int64) & 0xFFFF).sum().item())
+            rate = s / (ms * 1e-3) / 1e9
+            peak = SM_COUNT * FP32_LANES_PER_SM * f_max * 1e6 / FIG4_OPS[name] / 1e9
+            res[key] = {
+                "ms": ms, "gpix_iter_s": rate, "pixel_iters": s, "frames_per_s": 1e3 / ms,
+                "fp32_ops_per_iter": FIG4_OPS[name], "frac_of_fp32_pipe": rate / peak,
+                "note": "kernel S (one orbit per lane, strict sequence)"
+                        + ("; the two divisions are counted as one op each" if "RAT" in name
+                           else "")}
+        del out
+    except Exception as e:  # report, never fail the line
+        res["error"] = f"{type(e).__name__}: {e}"[:300]
     return res
 
 
@@ -680,7 +731,7 @@ def cardioid_path_rate(fr, W, torch, f_max):
                 "gpix_iter_s": s / (ms * 1e-3) / 1e9,
                 "mean_iters_per_px": s / (len(cs) * W_PX * H_PX),
                 "frac_of_alu_peak": s / (ms * 1e-3) / 1e9 / peak,
-                "note": "cardioid a = 3.9, clockwise (fr_cardioid_path), kernel S"}
+                "note": "cardioid a = 3.9, clockwise (fr_cardioid_path), kernel SX"}
     except Exception as e:  # report, never fail the line
         return {"error": f"{type(e).__name__}: {e}"[:300]}
 

@@ -318,6 +318,9 @@ struct Ops<double> {
   __device__ __forceinline__ static double inf() { return __longlong_as_double(0x7ff0000000000000ll); }
 };
 
+#ifndef FR_FN_FREEZE
+#define FR_FN_FREEZE 1
+#endif
 template <class T, int FN>
 struct FnIter {
   __device__ __forceinline__ static void step(T& x, T& y, T cr, T ci, unsigned& alive, int& cnt) {
@@ -325,6 +328,10 @@ struct FnIter {
     const T xx = O::mul(x, x);
     const T yy = O::mul(y, y);
     O::alive(alive, cnt, O::add(xx, yy));
+    // the rational map: an escaped lane stops here -- its count is final, and its orbit
+    // would run to inf / NaN within a few iterations, where every IEEE division of the
+    // warp takes the slow path (FR_FN_FREEZE=0 keeps iterating, for the A/B)
+    if (FN == 2 && FR_FN_FREEZE && !alive) return;
     const T xy = O::mul(x, y);
     const T wx = O::sub(xx, yy);
     const T wy = O::add(xy, xy);

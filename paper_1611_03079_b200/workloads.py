@@ -45,6 +45,11 @@ FIG2_C = (0.320564 - 0.0391827j, -0.454038 - 0.572187j, -0.763667 + 0.0870413j,
 FIG3_C = (0.177078 + 0.577384j, 0.185723 + 0.588104j)
 # Figure 4: the alternate-function parameter (NEXT-3; not on the hot path).
 FIG4_C = 0.862085 + 0.64695j
+# "zoom on Julia set" (Figure 4 caption): the paper gives no window; this 1080p zoom on
+# the rational map's set boundary (centre 0.65625+0.65625i, real span 0.375) is chosen
+# for orbits of cfg4-like length (mean count ~15, ~7% interior at max_iter 100).
+FIG4_ZOOM_CENTER = 0.65625 + 0.65625j
+FIG4_ZOOM_SPAN = 0.375
 # Cardioid path divisor: a = 3.9 (a = 4 is the main-cardioid border).
 CARDIOID_A = 3.9
 
