@@ -40,7 +40,7 @@ def _fast_f32(name):
     # escape_tile / escape_refill / escape_budget / escape_cont kernels with T = float,
     # STRICT = false; escape_tile2_kernel<STRICT = false, ...>
     return (re.search(r"escape_(tile|refill|budget|cont)_kernelIfLb0E", name) is not None
-            or "escape_tile2_kernelILb0E" in name)
+            or "escape_tile2_kernelILb0E" in name or "escape_pathx_kernel" in name)
 
 
 def test_sm100a(sass):
@@ -104,8 +104,49 @@ def test_fast_two_orbit_loops_are_packed(sass):
     names = [n for n in funcs
              if "escape_tile2_kernelILb0E" in n
              or re.search(r"escape_budget_kernelIfLb0ELb[01]ELb[01]ELi0ELi0E", n)
-             or re.search(r"escape_tile_kernelIfLb0ELb0ELb[01]ELi4ELi1024E", n)]
-    assert len(names) >= 6
+             or re.search(r"escape_tile_kernelIfLb0ELb0ELb[01]ELi4ELi1024E", n)
+             or "escape_pathx_kernel" in n]
+    assert len(names) >= 14
     for name in names:
         assert sum("FFMA2" in i for i in funcs[name]) >= 8, name
         assert any("FMUL2" in i for i in funcs[name]), name
+
+
+def _loops(ins):
+    """Backward-branch loops of a function's SASS: (first, last) index pairs."""
+    addr = []
+    for i in ins:
+        m = re.match(r"/\*([0-9a-f]{4,})\*/", i)
+        addr.append(int(m.group(1), 16) if m else None)
+    out = []
+    for k, i in enumerate(ins):
+        m = re.search(r"BRA (?:P\d, )?0x([0-9a-f]+)", i)
+        if m and addr[k] is not None and int(m.group(1), 16) < addr[k]:
+            t = int(m.group(1), 16)
+            first = next(j for j, a in enumerate(addr) if a is not None and a >= t)
+            out.append((first, k))
+    return out
+
+
+def test_sx_frame_loop_vote_blocks_are_move_free(sass):
+    """Kernel SX's uint16 PTX frame loop: every vote loop of the bench
+    kernel is the 23-instruction packed block -- 10 FFMA2/FMUL2, 4 FSETP, 4 count
+    increments, vote, loop test -- with no register moves.  Register budgets that make
+    ptxas add 2-3 moves per block measured 4-10% slower (profiles/r02/ab_sx_regs.txt)."""
+    _, funcs = sass
+    raw = subprocess.run(["cuobjdump", "-sass", build.LIB], capture_output=True, text=True,
+                         check=True).stdout
+    name = next(n for n in funcs if re.search(r"escape_pathx_kernelILi1024ELi2ELb0ELb1E", n))
+    body = raw.split("Function : " + name, 1)[1].split("Function :", 1)[0]
+    ins = [re.sub(r"/\*\s*0x[0-9a-f]+\s*\*/", "", l).strip() for l in body.splitlines()]
+    ins = [i for i in ins if re.match(r"/\*[0-9a-f]{4,}\*/", i)]
+    # innermost vote loops: one VOTE, no store (the frame loop around them has both)
+    vote_loops = [(a, b) for a, b in _loops(ins)
+                  if sum("VOTE" in x for x in ins[a:b + 1]) == 1
+                  and not any("STG" in x for x in ins[a:b + 1])]
+    assert vote_loops, name
+    for a, b in vote_loops:
+        blk = ins[a:b + 1]
+        assert sum(bool(re.search(r"\b(FFMA2|FMUL2)\b", x)) for x in blk) == 10, blk
+        assert not [x for x in blk if re.search(r"\bMOV\b|IMAD\.MOV", x)], blk
+        assert len(blk) <= 23, (len(blk), blk)
