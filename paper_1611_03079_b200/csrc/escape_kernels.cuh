@@ -43,6 +43,19 @@ constexpr int kWarpH = 4;
 constexpr int kMaxPathChunk = 1024;  // C values per launch, carried in kernel params
 constexpr unsigned kFull = 0xffffffffu;
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the PDL attribute may
+// start while the previous kernel of its stream is still finishing.  pdl_trigger() lets
+// the NEXT kernel's CTAs start launching; pdl_wait() blocks until the previous kernel
+// has completed and its memory is visible -- every kernel that uses them calls
+// pdl_wait() before its first global-memory access other than its parameters, so the
+// overlap covers only work that touches nothing the previous kernel writes.  Both are
+// no-ops when the kernel was launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+
 // ----------------------------------------------------------------------------------
 // Parameters (passed by value; the path chunk's C values ride in param space).
 // ----------------------------------------------------------------------------------
@@ -870,6 +883,7 @@ __global__ void __launch_bounds__(kThreads)
 escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int frame0,
                    int n_frames, int fpc) {
   static_assert(FN == 0 || (STRICT && !MANDEL), "map variants: strict Julia frames");
+  if constexpr (NC == 1) pdl_trigger();
   static_assert(ES == 1 || ES == 2, "counts are uint16 (ES 2) or uint8 (ES 1)");
   using CountT = typename std::conditional<ES == 2, uint16_t, uint8_t>::type;
   __shared__ uint32_t spal[COLOR ? 256 : 1];
@@ -1008,6 +1022,7 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
     if (kfull != max_iter && n == kfull && __any_sync(kFull, alive)) {
       for (; n < max_iter; ++n) It::step(x, y, cr, ci, alive, cnt);
     }
+    if constexpr (NC == 1) pdl_wait();  // single frames are launched with PDL
     if (inside) {
       const int count = cnt;  // <= max_iter (see above)
       put(outp, count, 0);
@@ -1207,6 +1222,7 @@ __global__ void __launch_bounds__(kThreads)
 escape_tile2_kernel(const Geom g, const PalRef pal, const float jcr2, const float jci2) {
   // jcr2/jci2: the Julia C in the state representation (doubled in FAST, plain in STRICT)
   // colours from the device palette (no CTA barrier in these short-lived CTAs)
+  pdl_trigger();  // the next frame's CTAs may start while this frame's last wave runs
   int tx, ty, grp;
   tile_of(g, tx, ty, grp);
   const int lane = threadIdx.x & 31;
@@ -1250,6 +1266,7 @@ escape_tile2_kernel(const Geom g, const PalRef pal, const float jcr2, const floa
       }
     }
   }
+  pdl_wait();  // stores (and palette reads) only after the previous kernel completed
   if (in0) {
     const int64_t off = (int64_t)ly0 * g.W + px;
     const int c0 = cnt;  // <= max_iter: at most one increment per executed iteration

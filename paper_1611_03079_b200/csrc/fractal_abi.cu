@@ -199,6 +199,28 @@ dim3 tile_grid(fr::Geom& g, int64_t tiles_y, int groups) {
   return dim3((unsigned)((int64_t)g.tiles_x * tiles_y), (unsigned)groups, 1);
 }
 
+// Launch with programmatic dependent launch (PDL): the kernel may start
+// while the previous kernel of the stream finishes; it calls pdl_wait() before touching
+// global memory.  FRACTAL_PDL=0 launches plainly (A/B).
+bool pdl_on() {
+  static const bool on = !env_is("FRACTAL_PDL", "0");
+  return on;
+}
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(fr::kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int NC>
 cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr::CList<T, NC>& cs,
                            int n_frames, int frame0, cudaStream_t s) {
@@ -215,9 +237,10 @@ cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr:
       if constexpr (!STRICT) {
         if (vote_k() == 2) k2 = fr::escape_tile2_kernel<STRICT, MANDEL, COLOR, 2>;
       }
-      k2<<<grid2, fr::kThreads, 0, s>>>(g, pal_ref(pal), cs.re[0], cs.im[0]);
+      const cudaError_t e =
+          launch_pdl(k2, grid2, s, g, pal_ref(pal), cs.re[0], cs.im[0]);
       g_launches.fetch_add(1, std::memory_order_relaxed);
-      return cudaGetLastError();
+      return e;
     }
   }
   // C-path frames in FP32_FAST: kernel SX (x-adjacent pixel pairs, whole-sector count
@@ -259,6 +282,11 @@ cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr:
           <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);
     else
       return cudaErrorInvalidValue;
+  } else if constexpr (NC == 1) {  // single frames: PDL (the kernel waits before storing)
+    const cudaError_t e = launch_pdl(fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, KD, NC>,
+                                     grid, s, g, pal, cs, frame0, n_frames, fpc);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return e;
   } else {
     fr::escape_tile_kernel<T, STRICT, MANDEL, COLOR, KD, NC>
         <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, frame0, n_frames, fpc);
@@ -806,10 +834,11 @@ cudaError_t launch_fn_t(const fr::Geom& g0, const fr::Palette& pal, fr_complex c
   cs.re[0] = state_of<T, true>(c.re);
   cs.im[0] = state_of<T, true>(c.im);
   const dim3 grid = tile_grid(g, (g.rows + fr::kTileH - 1) / fr::kTileH, 1);
-  fr::escape_tile_kernel<T, true, false, COLOR, 4, 1, FN>
-      <<<grid, fr::kThreads, 0, s>>>(g, pal, cs, 0, 1, 1);
+  const cudaError_t e =
+      launch_pdl(fr::escape_tile_kernel<T, true, false, COLOR, 4, 1, FN>, grid, s, g, pal, cs,
+                 0, 1, 1);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  return e;
 }
 
 template <int FN>
