@@ -60,6 +60,11 @@
  *           calls on one stream share its workspaces in stream order); apart from
  *           those caches the library holds only a monotonic launch counter
  *           (fr_launch_count).
+ *  Overlap. Single-frame kernels use programmatic dependent launch: when the
+ *           previous operation on `stream` is one of this library's single-frame
+ *           kernels, the next one may start computing before it has finished, but
+ *           touches no global memory until it has completed, so stream order holds
+ *           for every memory effect (FRACTAL_PDL=0 in the environment disables it).
  *  Stream.  `stream` is a cudaStream_t (NULL = legacy default stream).
  */
 #ifndef FRACTAL_H_
