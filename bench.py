@@ -601,7 +601,9 @@ def extras(fr, W, torch):
             def fn():
                 fr.mandelbrot_param_map(cfg.window, cfg.width, cfg.height, cfg.max_iter, mode,
                                         out=out)
-        reps = 2 if name == "cfg5" else 50
+        # timed regions of several ms: a sub-ms burst after an idle sync is ~1 us per call
+        # slower on cfg2 (clock ramp at the burst's start)
+        reps = {"cfg2": 400, "cfg3": 50, "cfg5": 2}[name]
         fn()
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
@@ -684,7 +686,7 @@ def fig4_maps_rate(fr, W, torch, f_max):
             torch.cuda.synchronize()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
-            reps = 20
+            reps = 200
             a.record()
             for _ in range(reps):
                 call()
