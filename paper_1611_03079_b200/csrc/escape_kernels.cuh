@@ -1088,8 +1088,14 @@ constexpr int kTileWX = 64;
 constexpr int kSxChunk = 128;  // frames per shared-memory C chunk
 // VEC (host-checked): even width and frame stride, aligned outputs -- both pixels of a
 // lane are in or out together and every pair store is aligned
+#ifndef FR_SX_WARPS  // warps per CTA of kernel SX: 4 (CTA tile 64 x 4; bench 2.322 -> 2.293 ms) or 8
+#define FR_SX_WARPS 4
+#endif
+constexpr int kSxThreads = 32 * FR_SX_WARPS;
+constexpr int kSxRows = FR_SX_WARPS == 8 ? 8 : 4;  // CTA tile rows
+static_assert(FR_SX_WARPS == 8 || FR_SX_WARPS == 4, "kernel SX: 4 or 8 warps per CTA");
 template <int NC, int ES, bool COLOR, bool VEC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kSxThreads)
 escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, int frame0,
                     int n_frames, int fpc) {
   using CountT = typename std::conditional<ES == 2, uint16_t, uint8_t>::type;
@@ -1098,7 +1104,7 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int px = tx * kTileWX + (warp & 3) * 16 + (lane & 7) * 2;
-  const int ly = ty * kTileH + (warp >> 2) * 4 + (lane >> 3);
+  const int ly = ty * kSxRows + (warp >> 2) * 4 + (lane >> 3);
   const bool in0 = px < g.W && ly < g.rows;
   const bool in1 = px + 1 < g.W && ly < g.rows;
   const float re0 = to_state<float, false>(pixel_re(g, min(px, g.W - 1)));
@@ -1185,7 +1191,7 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
       for (int c0 = f0; c0 < f1; c0 += kSxChunk) {
         const int nc = min(kSxChunk, f1 - c0);
         __syncthreads();
-        for (int i = threadIdx.x; i < nc; i += kThreads) sc[i] = make_float2(cs.re[c0 + i], cs.im[c0 + i]);
+        for (int i = threadIdx.x; i < nc; i += kSxThreads) sc[i] = make_float2(cs.re[c0 + i], cs.im[c0 + i]);
         __syncthreads();
         sx_frames_u16(pre, static_cast<uint32_t>(__cvta_generic_to_shared(sc)), nc,
                       reinterpret_cast<uint32_t*>(outp), stride * 2, kfull, in0);

@@ -254,7 +254,7 @@ cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr:
       // profiles/r02/ab_sx_fpc.txt); FRACTAL_FPC overrides
       const int fpcx = fpc_env > 0 ? fpc : (n_frames < 64 ? n_frames : 64);
       const dim3 gridx =
-          tile_grid(gx, (g.rows + fr::kTileH - 1) / fr::kTileH, (n_frames + fpcx - 1) / fpcx);
+          tile_grid(gx, (g.rows + fr::kSxRows - 1) / fr::kSxRows, (n_frames + fpcx - 1) / fpcx);
       // VEC: both pixels of every lane pair in or out together, pair stores aligned
       const int es = g.counts8 != nullptr ? 1 : 2;
       const uintptr_t base_c = g.counts8 != nullptr ? reinterpret_cast<uintptr_t>(g.counts8)
@@ -266,7 +266,7 @@ cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr:
                            : fr::escape_pathx_kernel<NC, 1, COLOR, false>)
                     : (vec ? fr::escape_pathx_kernel<NC, 2, COLOR, true>
                            : fr::escape_pathx_kernel<NC, 2, COLOR, false>);
-      kx<<<gridx, fr::kThreads, 0, s>>>(gx, pal_ref(pal), cs, frame0, n_frames, fpcx);
+      kx<<<gridx, fr::kSxThreads, 0, s>>>(gx, pal_ref(pal), cs, frame0, n_frames, fpcx);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return cudaGetLastError();
     }
