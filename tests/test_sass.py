@@ -129,8 +129,8 @@ def _loops(ins):
 
 
 def test_sx_frame_loop_vote_blocks_are_move_free(sass):
-    """Kernel SX's uint16 PTX frame loop: every vote loop of the bench
-    kernel is the 23-instruction packed block -- 10 FFMA2/FMUL2, 4 FSETP, 4 count
+    """Kernel SX's uint16 PTX frame loop: every vote loop of its frame
+    loops is the 23-instruction packed block -- 10 FFMA2/FMUL2, 4 FSETP, 4 count
     increments, vote, loop test -- with no register moves.  Register budgets that make
     ptxas add 2-3 moves per block measured 4-10% slower (profiles/r02/ab_sx_regs.txt)."""
     _, funcs = sass
@@ -140,10 +140,19 @@ def test_sx_frame_loop_vote_blocks_are_move_free(sass):
     body = raw.split("Function : " + name, 1)[1].split("Function :", 1)[0]
     ins = [re.sub(r"/\*\s*0x[0-9a-f]+\s*\*/", "", l).strip() for l in body.splitlines()]
     ins = [i for i in ins if re.match(r"/\*[0-9a-f]{4,}\*/", i)]
-    # innermost vote loops: one VOTE, no store (the frame loop around them has both)
-    vote_loops = [(a, b) for a, b in _loops(ins)
+    # the PTX frame loop of the first C chunk (the one every frame group of <= 128 frames
+    # runs; nvcc unrolls the chunk loop, and later copies are not pinned): the first outer
+    # loop that loads C from shared memory (LDS) and stores; the innermost vote loops
+    # inside it (one VOTE, no store)
+    loops = _loops(ins)
+    frame_loops = [(a, b) for a, b in loops
+                   if any("LDS" in x for x in ins[a:b + 1]) and any("STG" in x for x in ins[a:b + 1])]
+    assert frame_loops, name
+    frame_loops = [min(frame_loops)]
+    vote_loops = [(a, b) for a, b in loops
                   if sum("VOTE" in x for x in ins[a:b + 1]) == 1
-                  and not any("STG" in x for x in ins[a:b + 1])]
+                  and not any("STG" in x for x in ins[a:b + 1])
+                  and any(fa <= a and b <= fb for fa, fb in frame_loops)]
     assert vote_loops, name
     for a, b in vote_loops:
         blk = ins[a:b + 1]
