@@ -1072,7 +1072,11 @@ escape_tile_kernel(const Geom g, const Palette pal, const CList<T, NC> cs, int f
 // The CTA renders a group of `fpc` frames of the path chunk for its tile (pixel map
 // amortised over the group), one frame at a time.
 // ----------------------------------------------------------------------------------
-constexpr int kTileWX = 64;
+#ifndef FR_SX_WARPS  // warps per CTA of kernel SX (see kSxThreads below)
+#define FR_SX_WARPS 4
+#endif
+constexpr int kSxWarpsX = FR_SX_WARPS < 4 ? FR_SX_WARPS : 4;  // warp tiles side by side
+constexpr int kTileWX = 16 * kSxWarpsX;                          // CTA tile width
 #ifndef FR_SX_UNROLL  // unroll the frame loop of kernel SX by 4 (A/B knob)
 #define FR_SX_UNROLL 0
 #endif
@@ -1088,12 +1092,12 @@ constexpr int kTileWX = 64;
 constexpr int kSxChunk = 128;  // frames per shared-memory C chunk
 // VEC (host-checked): even width and frame stride, aligned outputs -- both pixels of a
 // lane are in or out together and every pair store is aligned
-#ifndef FR_SX_WARPS  // warps per CTA of kernel SX: 4 (CTA tile 64 x 4; bench 2.322 -> 2.293 ms) or 8
-#define FR_SX_WARPS 4
-#endif
+// warps per CTA of kernel SX: 4 (CTA tile 64 x 4; bench 2.322 -> 2.293 ms against 8,
+// profiles/r02/ab_sx_warps.txt), 8 (64 x 8) or 2 (32 x 4)
 constexpr int kSxThreads = 32 * FR_SX_WARPS;
-constexpr int kSxRows = FR_SX_WARPS == 8 ? 8 : 4;  // CTA tile rows
-static_assert(FR_SX_WARPS == 8 || FR_SX_WARPS == 4, "kernel SX: 4 or 8 warps per CTA");
+constexpr int kSxRows = 4 * (FR_SX_WARPS / kSxWarpsX);  // CTA tile rows
+static_assert(FR_SX_WARPS == 8 || FR_SX_WARPS == 4 || FR_SX_WARPS == 2,
+              "kernel SX: 2, 4 or 8 warps per CTA");
 template <int NC, int ES, bool COLOR, bool VEC>
 __global__ void __launch_bounds__(kSxThreads)
 escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, int frame0,
@@ -1103,8 +1107,8 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
   tile_of(g, tx, ty, grp);  // g.tiles_x counts 64-pixel tiles here
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int px = tx * kTileWX + (warp & 3) * 16 + (lane & 7) * 2;
-  const int ly = ty * kSxRows + (warp >> 2) * 4 + (lane >> 3);
+  const int px = tx * kTileWX + (warp % kSxWarpsX) * 16 + (lane & 7) * 2;
+  const int ly = ty * kSxRows + (warp / kSxWarpsX) * 4 + (lane >> 3);
   const bool in0 = px < g.W && ly < g.rows;
   const bool in1 = px + 1 < g.W && ly < g.rows;
   const float re0 = to_state<float, false>(pixel_re(g, min(px, g.W - 1)));
