@@ -250,9 +250,9 @@ cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr:
     if (sx) {
       fr::Geom gx = g;
       gx.tiles_x = (g.W + fr::kTileWX - 1) / fr::kTileWX;
-      // 64 frames per CTA (bench: 16/32/64/128 -> 2.80/2.73/2.70/2.72 ms,
-      // profiles/r02/ab_sx_fpc.txt); FRACTAL_FPC overrides
-      const int fpcx = fpc_env > 0 ? fpc : (n_frames < 64 ? n_frames : 64);
+      // 128 frames per CTA, one shared-memory C chunk (bench, 4-warp CTAs: 32/64/128/256
+      // -> 2.347/2.296/2.289/2.449 ms, profiles/r02/ab_sx_fpc_w4.txt); FRACTAL_FPC overrides
+      const int fpcx = fpc_env > 0 ? fpc : (n_frames < 128 ? n_frames : 128);
       const dim3 gridx =
           tile_grid(gx, (g.rows + fr::kSxRows - 1) / fr::kSxRows, (n_frames + fpcx - 1) / fpcx);
       // VEC: both pixels of every lane pair in or out together, pair stores aligned
