@@ -1227,8 +1227,14 @@ escape_pathx_kernel(const Geom g, const PalRef pal, const CList<float, NC> cs, i
 // both, half the per-pixel overhead).  Julia frames share C; Mandelbrot maps take each
 // orbit's C from its pixel (Z_0 = 0).  Bit-identical to kernel S (same arithmetic).
 // ----------------------------------------------------------------------------------
+#ifndef FR_S2_WARPS  // warps per CTA of kernel S2: 8 (tile 32 x 16) or 4 (half of one; cfg2
+                     // 17.5 -> 17.9 us per call, profiles/r02/ab_s2_warps.txt)
+#define FR_S2_WARPS 8
+#endif
+constexpr int kS2Threads = 32 * FR_S2_WARPS;
+static_assert(FR_S2_WARPS == 8 || FR_S2_WARPS == 4, "kernel S2: 4 or 8 warps per CTA");
 template <bool STRICT, bool MANDEL, bool COLOR, int KV = 4>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kS2Threads)
 escape_tile2_kernel(const Geom g, const PalRef pal, const float jcr2, const float jci2) {
   // jcr2/jci2: the Julia C in the state representation (doubled in FAST, plain in STRICT)
   // colours from the device palette (no CTA barrier in these short-lived CTAs)
@@ -1237,8 +1243,11 @@ escape_tile2_kernel(const Geom g, const PalRef pal, const float jcr2, const floa
   tile_of(g, tx, ty, grp);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  // 4-warp CTAs: grid rows count half tiles; the low bit picks the warp-tile row
+  const int wy = FR_S2_WARPS == 8 ? (warp >> 2) : (ty & 1);
+  if (FR_S2_WARPS == 4) ty >>= 1;
   const int cx = (warp & 3) * kWarpW + (lane & 7);
-  const int cy = (warp >> 2) * kWarpH + (lane >> 3);
+  const int cy = wy * kWarpH + (lane >> 3);
   const int px = tx * kTileW + cx;
   const int ly0 = ty * (2 * kTileH) + cy;
   const int ly1 = ly0 + kTileH;

@@ -207,10 +207,11 @@ bool pdl_on() {
   return on;
 }
 template <class... KArgs, class... Args>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, cudaStream_t s, Args&&... args) {
+cudaError_t launch_pdl_n(void (*kernel)(KArgs...), dim3 grid, unsigned threads, cudaStream_t s,
+                         Args&&... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(fr::kThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -219,6 +220,10 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, cudaStream_t s, Args
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, cudaStream_t s, Args&&... args) {
+  return launch_pdl_n(kernel, grid, fr::kThreads, s, std::forward<Args>(args)...);
 }
 
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int NC>
@@ -232,13 +237,14 @@ cudaError_t launch_tiles_t(const fr::Geom& g0, const fr::Palette& pal, const fr:
   static const bool s2 = !env_is("FRACTAL_S2", "0");
   if constexpr (NC == 1 && std::is_same<T, float>::value) {
     if (s2 && g.counts8 == nullptr) {
-      const dim3 grid2 = tile_grid(g, (g.rows + 2 * fr::kTileH - 1) / (2 * fr::kTileH), 1);
+      const dim3 grid2 =
+          tile_grid(g, (g.rows + 2 * fr::kTileH - 1) / (2 * fr::kTileH) * (8 / FR_S2_WARPS), 1);
       auto k2 = fr::escape_tile2_kernel<STRICT, MANDEL, COLOR>;
       if constexpr (!STRICT) {
         if (vote_k() == 2) k2 = fr::escape_tile2_kernel<STRICT, MANDEL, COLOR, 2>;
       }
       const cudaError_t e =
-          launch_pdl(k2, grid2, s, g, pal_ref(pal), cs.re[0], cs.im[0]);
+          launch_pdl_n(k2, grid2, fr::kS2Threads, s, g, pal_ref(pal), cs.re[0], cs.im[0]);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return e;
     }
