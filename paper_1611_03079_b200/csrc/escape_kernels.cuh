@@ -2303,6 +2303,59 @@ colorize_kernel(const uint16_t* __restrict__ counts, int64_t n_pixels, int max_i
   if (blockIdx.x == 0 && t < n_pixels) rgba[t] = colour_of(spal, pal, counts[t], max_iter);
 }
 
+// Variant with warp-contiguous stores: a warp handles blocks of 256 pixels, lane l the
+// pixels 4l..4l+3 and 128+4l..128+4l+3, so each 16-byte store instruction of the warp
+// covers 512 contiguous bytes (whole lines) and each 8-byte load 256 contiguous bytes
+// (the kernel above stores 16 bytes per lane at a 32-byte stride).  FR_COLORIZE_V2 picks it.
+__global__ void __launch_bounds__(kThreads)
+colorize_kernel2(const uint16_t* __restrict__ counts, int64_t n_pixels, int max_iter,
+                 const Palette pal, uint32_t* __restrict__ rgba) {
+  __shared__ uint32_t spal[256];
+  spal[threadIdx.x] = pal.e[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nblk = n_pixels >> 8;
+  const uint2* __restrict__ c4 = reinterpret_cast<const uint2*>(counts);
+  uint4* __restrict__ o4 = reinterpret_cast<uint4*>(rgba);
+  auto col4 = [&](const uint2 v) {
+    return make_uint4(colour_of(spal, pal, (int)(v.x & 0xffffu), max_iter),
+                      colour_of(spal, pal, (int)(v.x >> 16), max_iter),
+                      colour_of(spal, pal, (int)(v.y & 0xffffu), max_iter),
+                      colour_of(spal, pal, (int)(v.y >> 16), max_iter));
+  };
+  int64_t b = (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5);
+#ifndef FR_COLORIZE_U
+#define FR_COLORIZE_U 4
+#endif
+  constexpr int U = FR_COLORIZE_U;
+  for (; b + (U - 1) * nwarps < nblk; b += U * nwarps) {
+    uint2 va[U], vb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = (b + u * nwarps) * 64 + lane;
+      va[u] = __ldcs(c4 + q);
+      vb[u] = __ldcs(c4 + q + 32);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = (b + u * nwarps) * 64 + lane;
+      __stcs(o4 + q, col4(va[u]));
+      __stcs(o4 + q + 32, col4(vb[u]));
+    }
+  }
+  for (; b < nblk; b += nwarps) {
+    const int64_t q = b * 64 + lane;
+    const uint2 va = __ldcs(c4 + q), vb = __ldcs(c4 + q + 32);
+    __stcs(o4 + q, col4(va));
+    __stcs(o4 + q + 32, col4(vb));
+  }
+  // ragged tail (< 256 pixels)
+  for (int64_t t = (nblk << 8) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_pixels;
+       t += (int64_t)gridDim.x * blockDim.x)
+    rgba[t] = colour_of(spal, pal, counts[t], max_iter);
+}
+
 // Unaligned fallback (pointers not 16-byte aligned): one pixel per thread-step.
 __global__ void __launch_bounds__(kThreads)
 colorize_scalar_kernel(const uint16_t* __restrict__ counts, int64_t n_pixels, int max_iter,

@@ -1031,6 +1031,9 @@ fr_status julia_render_path_host(const fr_complex* c_host, int32_t n_frames, fr_
   return cuda_status(e);
 }
 
+#ifndef FR_COLORIZE_V2  // warp-contiguous stores (colorize_kernel2); 0 = the first kernel
+#define FR_COLORIZE_V2 1
+#endif
 fr_status colorize(const uint16_t* counts, int64_t n_pixels, int32_t max_iter,
                    const fr_palette* pal, uint8_t* out_rgba, fr_stream stream) {
   if (n_pixels < 0 || max_iter < 1) return FR_ERR_INVALID_ARG;
@@ -1047,11 +1050,18 @@ fr_status colorize(const uint16_t* counts, int64_t n_pixels, int32_t max_iter,
   const bool aligned = ((uintptr_t)counts % 16 == 0) && ((uintptr_t)out_rgba % 16 == 0);
   const int64_t work = aligned ? (n_pixels >> 3) : n_pixels;
   int64_t blocks = (work + fr::kThreads - 1) / fr::kThreads;
-  const int64_t cap = (int64_t)sms * 8;
+  // grid cap: 512 CTAs per SM of the warp-contiguous kernel (1.06e9 pixels: 8/64/256/512/
+  // 1024 -> 0.83/0.96/0.995/1.00/0.93 of the HBM copy peak, profiles/r02/ab_colorize.txt;
+  // the old kernel at 8: 0.79); FRACTAL_COLORIZE_CTAS overrides (tests force grid strides)
+  static const int ctas_env = env_int("FRACTAL_COLORIZE_CTAS", 0);
+  const int64_t cap = (int64_t)sms * (ctas_env > 0 ? ctas_env : (FR_COLORIZE_V2 ? 512 : 8));
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   uint32_t* o = reinterpret_cast<uint32_t*>(out_rgba);
-  if (aligned)
+  if (aligned && FR_COLORIZE_V2)
+    fr::colorize_kernel2<<<(unsigned)blocks, fr::kThreads, 0, stream>>>(counts, n_pixels,
+                                                                         max_iter, p, o);
+  else if (aligned)
     fr::colorize_kernel<<<(unsigned)blocks, fr::kThreads, 0, stream>>>(counts, n_pixels,
                                                                         max_iter, p, o);
   else

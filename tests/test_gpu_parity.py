@@ -425,6 +425,38 @@ def test_colorize_standalone(fr, n, offset):
     np.testing.assert_array_equal(got.cpu().numpy(), oracle.colorize(counts[offset:], 1000, *odd))
 
 
+_COLORIZE_GRID = r"""
+import numpy as np, torch, sys
+import oracle
+from paper_1611_03079_b200 import binding as fr
+from paper_1611_03079_b200 import workloads as W
+n = 3 * (1 << 20) + 4321  # > 4 blocks of 256 pixels per warp of the forced 1-CTA/SM grid
+rng = np.random.default_rng(5)
+counts = rng.integers(0, 1001, size=n).astype(np.uint16)
+counts[::89] = 1000
+t = torch.from_numpy(counts.view(np.int16)).cuda().view(torch.uint16)
+pal = W.palette("fire")
+rgba = fr.colorize(t, 1000, pal)
+torch.cuda.synchronize()
+ok = np.array_equal(rgba.cpu().numpy().reshape(-1, 4), oracle.colorize(counts, 1000, *pal).reshape(-1, 4))
+sys.exit(0 if ok else 1)
+"""
+
+
+@pytest.mark.parametrize("ctas", ["1", "3"])
+def test_colorize_grid_stride(ctas):
+    """The warp-contiguous colorize kernel with a forced small grid (FRACTAL_COLORIZE_CTAS):
+    every warp runs its unrolled 4-block loop, the remainder loop and the ragged tail."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, FRACTAL_COLORIZE_CTAS=ctas)
+    r = subprocess.run([sys.executable, "-c", _COLORIZE_GRID], cwd=root, env=e,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("name,mode,pal_name", [("cfg2", "FP32_FAST", "fire"),
                                                ("cfg3", "FP32_FAST", "classic"),
                                                ("cfg3", "FP64_STRICT", "fire")])
