@@ -1,7 +1,7 @@
 """Every kernel family, whatever the default dispatch picks: a parity subset re-run in
 subprocesses with FRACTAL_SCHED forced to static (kernel S), refill (kernel R), amort
-(kernel A) and twophase (kernels P1 + P2, at several phase-1 budgets), and with the
-persistent / CTA-local refill grids."""
+(kernel A) and twophase (kernels P1 + P2, at several phase-1 budgets), with the
+persistent / CTA-local refill grids, and with programmatic dependent launch off."""
 import os
 import subprocess
 import sys
@@ -23,7 +23,8 @@ SUBSET = ("test_strict_configs_full_frame or test_strict_fuzz or test_strict_rag
                                   "FRACTAL_P2_OCC": "1"},
                                  {"FRACTAL_SCHED": "twophase", "FRACTAL_P1_TILES": "2"},
                                  {"FRACTAL_SCHED": "refill", "FRACTAL_REFILL_CPC": "16"},
-                                 {"FRACTAL_SCHED": "amort", "FRACTAL_REFILL_CPC": "0"}])
+                                 {"FRACTAL_SCHED": "amort", "FRACTAL_REFILL_CPC": "0"},
+                                 {"FRACTAL_PDL": "0"}])
 def test_parity_under_forced_scheduler(env):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
