@@ -1300,6 +1300,67 @@ escape_tile2_kernel(const Geom g, const PalRef pal, const float jcr2, const floa
   }
 }
 
+// ----------------------------------------------------------------------------------
+// Figure 4 maps (FnIter, the strict sequence; NEXT-3) on the S2 layout: CTA tile 32 x 16,
+// two pixels per thread (rows y and y + 8) iterated together for instruction-level
+// parallelism across the long dependent chain of the rational map's divisions.
+// ----------------------------------------------------------------------------------
+template <class T, int FN, bool COLOR>
+__global__ void __launch_bounds__(kThreads)
+escape_fn2_kernel(const Geom g, const Palette pal, const T jcr, const T jci) {
+  __shared__ uint32_t spal[COLOR ? 256 : 1];
+  if (COLOR) {
+    spal[threadIdx.x] = pal.e[threadIdx.x];
+    __syncthreads();
+  }
+  pdl_trigger();
+  int tx, ty, grp;
+  tile_of(g, tx, ty, grp);
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int px = tx * kTileW + (warp & 3) * kWarpW + (lane & 7);
+  const int ly0 = ty * (2 * kTileH) + (warp >> 2) * kWarpH + (lane >> 3);
+  const int ly1 = ly0 + kTileH;
+  const bool in0 = (px < g.W) && (ly0 < g.rows);
+  const bool in1 = (px < g.W) && (ly1 < g.rows);
+  T x = to_state<T, true>(pixel_re(g, min(px, g.W - 1)));
+  T y = to_state<T, true>(pixel_im(g, global_row(g, min(ly0, g.rows - 1))));
+  T x2 = x;
+  T y2 = to_state<T, true>(pixel_im(g, global_row(g, min(ly1, g.rows - 1))));
+  unsigned alive = in0 ? 1u : 0u, alive2 = in1 ? 1u : 0u;
+  int cnt = 0, cnt2 = 0;
+  const int max_iter = g.max_iter;
+  const int kfull = max_iter - max_iter % 4;
+  using It = FnIter<T, FN>;
+  int n = 0;
+  while (n < kfull) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      It::step(x, y, jcr, jci, alive, cnt);
+      It::step(x2, y2, jcr, jci, alive2, cnt2);
+    }
+    n += 4;
+    if (!__any_sync(kFull, alive | alive2)) break;
+  }
+  if (kfull != max_iter && n == kfull && __any_sync(kFull, alive | alive2)) {
+    for (; n < max_iter; ++n) {
+      It::step(x, y, jcr, jci, alive, cnt);
+      It::step(x2, y2, jcr, jci, alive2, cnt2);
+    }
+  }
+  pdl_wait();
+  if (in0) {
+    const int64_t off = (int64_t)ly0 * g.W + px;
+    g.counts[off] = (uint16_t)cnt;
+    if (COLOR) g.rgba[off] = colour_of(spal, pal, cnt, max_iter);
+  }
+  if (in1) {
+    const int64_t off = (int64_t)ly1 * g.W + px;
+    g.counts[off] = (uint16_t)cnt2;
+    if (COLOR) g.rgba[off] = colour_of(spal, pal, cnt2, max_iter);
+  }
+}
+
 // Optional per-warp timeline of kernels R and P2 (diagnostics; null in normal operation):
 // [warp][0] = %globaltimer at entry, [1] = at chunk-supply exhaustion, [2] = at exit.
 __device__ unsigned long long* g_refill_trace = nullptr;

@@ -839,10 +839,18 @@ cudaError_t launch_fn_t(const fr::Geom& g0, const fr::Palette& pal, fr_complex c
   fr::CList<T, 1> cs;
   cs.re[0] = state_of<T, true>(c.re);
   cs.im[0] = state_of<T, true>(c.im);
-  const dim3 grid = tile_grid(g, (g.rows + fr::kTileH - 1) / fr::kTileH, 1);
-  const cudaError_t e =
-      launch_pdl(fr::escape_tile_kernel<T, true, false, COLOR, 4, 1, FN>, grid, s, g, pal, cs,
-                 0, 1, 1);
+#ifndef FR_FN2  // z^4 + c on the two-pixel S2 layout (escape_fn2_kernel; the rational map
+#define FR_FN2 1  // measured slower there: profiles/r02/ab_fig4_fn2.txt)
+#endif
+  cudaError_t e;
+  if constexpr (FR_FN2 && FN == 1) {
+    const dim3 grid2 = tile_grid(g, (g.rows + 2 * fr::kTileH - 1) / (2 * fr::kTileH), 1);
+    e = launch_pdl(fr::escape_fn2_kernel<T, FN, COLOR>, grid2, s, g, pal, cs.re[0], cs.im[0]);
+  } else {
+    const dim3 grid = tile_grid(g, (g.rows + fr::kTileH - 1) / fr::kTileH, 1);
+    e = launch_pdl(fr::escape_tile_kernel<T, true, false, COLOR, 4, 1, FN>, grid, s, g, pal, cs,
+                   0, 1, 1);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return e;
 }

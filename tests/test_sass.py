@@ -76,8 +76,10 @@ def _tile_fn_param(name):
 
 
 def _strict(name):
+    # escape_fn2_kernel: the Figure 4 map z^4 + c (FN = 1), strict sequence only
     return (re.search(r"escape_(tile|refill|budget|cont)_kernelI[fd]Lb1E", name) is not None
-            or "escape_tile2_kernelILb1E" in name)
+            or "escape_tile2_kernelILb1E" in name
+            or re.search(r"escape_fn2_kernelI[fd]Li1E", name) is not None)
 
 
 def test_strict_kernels_never_fuse(sass):
