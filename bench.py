@@ -699,9 +699,9 @@ def fig4_maps_rate(fr, W, torch, f_max):
             res[key] = {
                 "ms": ms, "gpix_iter_s": rate, "pixel_iters": s, "frames_per_s": 1e3 / ms,
                 "fp32_ops_per_iter": FIG4_OPS[name], "frac_of_fp32_pipe": rate / peak,
-                "note": "kernel S (one orbit per lane, strict sequence)"
-                        + ("; the two divisions are counted as one op each" if "RAT" in name
-                           else "")}
+                "note": ("kernel S (one orbit per lane, strict sequence); the two divisions "
+                         "are counted as one op each" if "RAT" in name else
+                         "kernel fn2 (two pixels per thread, strict sequence)")}
         del out
     except Exception as e:  # report, never fail the line
         res["error"] = f"{type(e).__name__}: {e}"[:300]
