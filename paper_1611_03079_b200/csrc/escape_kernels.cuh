@@ -1414,6 +1414,10 @@ struct ContQueue {
 // replay per orbit, deferred to the end).
 // PRE > 0: the first PRE iterations run the exact vote loop (counts of the orbits that
 // end there are final); the amortised sub-blocks continue the rest from PRE.
+#ifndef FR_P1_WARPS  // warps per CTA of kernel P1: 4 (half of a 32 x 16 tile; cfg3 0.1554 ->
+#define FR_P1_WARPS 4  // 0.1544 ms against 8, profiles/r02/ab_p1_warps.txt) or 8
+#endif
+constexpr int kP1Threads = 32 * FR_P1_WARPS;
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int KS, int PRE, int KV>
 __device__ __forceinline__ void budget_tile(const Geom& g, const PalRef& pal, const T jcr,
                                             const T jci, int budget, ContQueue* q,
@@ -1423,8 +1427,11 @@ __device__ __forceinline__ void budget_tile(const Geom& g, const PalRef& pal, co
   // from the device palette: no CTA barrier in these short-lived CTAs.
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  // 4-warp CTAs (FR_P1_WARPS): the tile-row index counts half tiles, its low bit the row
+  const int wy = FR_P1_WARPS == 8 ? (warp >> 2) : (ty & 1);
+  const int tyt = FR_P1_WARPS == 8 ? ty : (ty >> 1);
   const int px = tx * kTileW + (warp & 3) * kWarpW + (lane & 7);
-  const int ly0 = ty * (2 * kTileH) + (warp >> 2) * kWarpH + (lane >> 3);
+  const int ly0 = tyt * (2 * kTileH) + wy * kWarpH + (lane >> 3);
   const int ly1 = ly0 + kTileH;
   const bool in0 = (px < g.W) && (ly0 < g.rows);
   const bool in1 = (px < g.W) && (ly1 < g.rows);
@@ -1622,7 +1629,7 @@ __device__ __forceinline__ void budget_tile(const Geom& g, const PalRef& pal, co
 // longer CTAs; the FRACTAL_P1_TILES experiment of DESIGN.md §5.1c)
 template <class T, bool STRICT, bool MANDEL, bool COLOR, int KS = 0, int PRE = 0, int KV = 4,
           int NT = 1>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kP1Threads)
 escape_budget_kernel(const Geom g, const PalRef pal, const T jcr, const T jci, int budget,
                      ContQueue* q, QItem<T>* items) {
   int tx, ty, grp;

@@ -542,8 +542,8 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   auto* items = static_cast<fr::QItem<T>*>(ip);
   // FRACTAL_P1_TILES=2: each P1 CTA renders two vertically adjacent tiles (exact P1 only)
   static const int p1nt = env_int("FRACTAL_P1_TILES", 1) == 2 ? 2 : 1;
-  const dim3 grid1 =
-      tile_grid(g, (g.rows + 2 * p1nt * fr::kTileH - 1) / (2 * p1nt * fr::kTileH), 1);
+  const dim3 grid1 = tile_grid(
+      g, (g.rows + 2 * p1nt * fr::kTileH - 1) / (2 * p1nt * fr::kTileH) * (8 / FR_P1_WARPS), 1);
   const int budget = twophase_budget(amort, sizeof(T) == 8);
   // amortised P1 under the same precondition as the amortised P2 (FRACTAL_P1_AMORT:
   // 0 = exact test, else sub-blocks of 4 or 8 when the budget is a multiple of it)
@@ -577,7 +577,7 @@ cudaError_t launch_twophase_t(const fr::Geom& g0, const fr::Palette& pal, double
   // the two-tile CTA is the exact P1 alone (it overrides the other P1 knobs): its grid
   // covers half as many tile rows
   if (p1nt == 2) kern1 = fr::escape_budget_kernel<T, STRICT, MANDEL, COLOR, 0, 0, 4, 2>;
-  kern1<<<grid1, fr::kThreads, 0, s>>>(g, pal_ref(pal), jcr, jci, budget, q, items);
+  kern1<<<grid1, fr::kP1Threads, 0, s>>>(g, pal_ref(pal), jcr, jci, budget, q, items);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   g_launches.fetch_add(1, std::memory_order_relaxed);
